@@ -1,0 +1,196 @@
+// k_elem.cu — HBM-bound row kernels of the hot path.
+//
+//   patch_to_bf16 : fp32 patches [rows][pp] -> bf16 GEMM operand [rows][KP] (zero K padding)
+//   embed_finish  : X0 = LN_pre(concat(cls, patches W_pe) + pos) in place, t := 1/N
+//   gather_ln     : A[m] = bf16(LN(src[rows[m]]))  — gather of recompute rows + LN1/LN2 (a5)
+//   rgather       : reused rows: Delta = X[row] - X[provrow] -> bf16 (Eq. 8) and the
+//                   reuse-cache read K_l,V_l[row] <- K_l,V_l[provrow] (a7)
+//   ln_post       : Z_f = LN_post(X_L[f][CLS])
+// One warp per row; lane j owns elements j, j+32, ... (coalesced 128 B per warp access);
+// LN statistics in fp32 with a fixed butterfly reduction order (deterministic).
+#include "common.cuh"
+#include "rv_internal.h"
+
+namespace rv {
+namespace {
+
+constexpr int ROWS_PER_CTA = 8;  // 8 warps
+
+template <int VPL>
+RV_DEV void load_row(const float* __restrict__ src, int D, int lane, float (&x)[VPL]) {
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int k = lane + 32 * j;
+    x[j] = k < D ? src[k] : 0.f;
+  }
+}
+
+template <int VPL>
+RV_DEV void layer_norm_regs(float (&x)[VPL], int D, int lane, const float* __restrict__ g,
+                            const float* __restrict__ b) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) s += x[j];
+  const float mean = warp_sum(s) / (float)D;
+  float v = 0.f;
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int k = lane + 32 * j;
+    const float d = k < D ? x[j] - mean : 0.f;
+    v += d * d;
+  }
+  const float rstd = rsqrtf(warp_sum(v) / (float)D + 1e-5f);
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int k = lane + 32 * j;
+    if (k < D) x[j] = (x[j] - mean) * rstd * __ldg(g + k) + __ldg(b + k);
+  }
+}
+
+__global__ void patch_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst,
+                                     long long rows, int pp, int KP) {
+  const long long total = rows * (long long)KP;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / KP;
+    const int c = (int)(i - r * KP);
+    dst[i] = __float2bfloat16_rn(c < pp ? src[r * pp + c] : 0.f);
+  }
+}
+
+template <int VPL>
+__global__ void embed_finish_kernel(float* __restrict__ X, const float* __restrict__ cls,
+                                    const float* __restrict__ pos, const float* __restrict__ g,
+                                    const float* __restrict__ b, float* __restrict__ pcls, int n,
+                                    int T, int D, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long rows = (long long)n * T;
+  for (long long r = blockIdx.x * (long long)ROWS_PER_CTA + warp; r < rows;
+       r += (long long)gridDim.x * ROWS_PER_CTA) {
+    const int tok = (int)(r % T);
+    float* row = X + r * D;
+    float x[VPL];
+    if (tok == 0) load_row<VPL>(cls, D, lane, x);
+    else load_row<VPL>(row, D, lane, x);          // patches @ W_pe written by the PE GEMM
+    float p[VPL];
+    load_row<VPL>(pos + (long long)tok * D, D, lane, p);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) x[j] += p[j];
+    layer_norm_regs<VPL>(x, D, lane, g, b);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int k = lane + 32 * j;
+      if (k < D) row[k] = x[j];
+    }
+    if (tok > 0 && lane == 0) pcls[(r / T) * N + (tok - 1)] = 1.0f / (float)N;  // layer-1 t
+  }
+}
+
+template <int VPL>
+__global__ void gather_ln_kernel(const float* __restrict__ src, const int* __restrict__ rows,
+                                 const int* __restrict__ count, int M_host, const float* __restrict__ g,
+                                 const float* __restrict__ b, bf16* __restrict__ dst, int D) {
+  const int M = count ? *count : M_host;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
+    const long long r = rows ? rows[m] : m;
+    float x[VPL];
+    load_row<VPL>(src + r * D, D, lane, x);
+    layer_norm_regs<VPL>(x, D, lane, g, b);
+    bf16* o = dst + (long long)m * D;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int k = lane + 32 * j;
+      if (k < D) o[k] = __float2bfloat16_rn(x[j]);
+    }
+  }
+}
+
+__global__ void rgather_kernel(const float* __restrict__ X, bf16* __restrict__ KV,
+                               const int* __restrict__ idxR, const int* __restrict__ provrow,
+                               const int* __restrict__ count, bf16* __restrict__ Ar, int D) {
+  const int M = *count;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
+    const long long r = idxR[m], p = provrow[m];
+    const float* xr = X + r * D;
+    const float* xp = X + p * D;
+    bf16* o = Ar + (long long)m * D;
+    for (int k = lane; k < D; k += 32) o[k] = __float2bfloat16_rn(xr[k] - xp[k]);
+    const uint4* src = reinterpret_cast<const uint4*>(KV + p * 2 * D);
+    uint4* dst = reinterpret_cast<uint4*>(KV + r * 2 * D);
+    for (int k = lane; k < (2 * D) / 8; k += 32) dst[k] = src[k];
+  }
+}
+
+template <int VPL>
+__global__ void ln_post_kernel(const float* __restrict__ X, const float* __restrict__ g,
+                               const float* __restrict__ b, float* __restrict__ emb, int n, int T,
+                               int D) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int f = blockIdx.x * ROWS_PER_CTA + warp; f < n; f += gridDim.x * ROWS_PER_CTA) {
+    float x[VPL];
+    load_row<VPL>(X + (long long)f * T * D, D, lane, x);
+    layer_norm_regs<VPL>(x, D, lane, g, b);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int k = lane + 32 * j;
+      if (k < D) emb[(long long)f * D + k] = x[j];
+    }
+  }
+}
+
+int grid_rows(long long rows) {
+  long long g = (rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+  if (g > 148 * 16) g = 148 * 16;
+  return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace
+
+cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP,
+                                 cudaStream_t s) {
+  long long total = rows * KP;
+  long long g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  patch_to_bf16_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(src, dst, rows, pp, KP);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g,
+                                const float* b, float* pcls, int n, int T, int D, int N, cudaStream_t s) {
+  const int grid = grid_rows((long long)n * T);
+  const int v = (D + 31) / 32;
+  if (v <= 2) embed_finish_kernel<2><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
+  else if (v <= 24) embed_finish_kernel<24><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
+  else embed_finish_kernel<32><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
+                             const float* g, const float* b, bf16* dst, int D, cudaStream_t s) {
+  const int grid = grid_rows(max_rows);
+  const int v = (D + 31) / 32;
+  if (v <= 2) gather_ln_kernel<2><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  else if (v <= 24) gather_ln_kernel<24><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  else gather_ln_kernel<32><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rgather(const float* X, bf16* KV, const int* idxR, const int* provrow, const int* count,
+                           int max_rows, bf16* Ar, int D, cudaStream_t s) {
+  rgather_kernel<<<grid_rows(max_rows), 256, 0, s>>>(X, KV, idxR, provrow, count, Ar, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
+                           cudaStream_t s) {
+  const int grid = grid_rows(n);
+  const int v = (D + 31) / 32;
+  if (v <= 2) ln_post_kernel<2><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
+  else if (v <= 24) ln_post_kernel<24><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
+  else ln_post_kernel<32><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
+  return cudaGetLastError();
+}
+
+}  // namespace rv

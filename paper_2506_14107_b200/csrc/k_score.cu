@@ -1,0 +1,198 @@
+// k_score.cu — reuse decision and stream compaction for one level-wave.
+//
+// score_kernel (SURVEY §8(a) a2+a3): one CTA per frame of the wave, one warp per patch token.
+//   Eq. 1  s_i = max over the available references of cos(T_cur_i, T_ref_i), fp32,
+//                  provider = argmax, ties -> past; cos = 0 on a zero norm (Q9)
+//   Eq. 2  v_i = [s_i, t_i, 1[I], 1[P], 1[B2], 1[B1], c_i]
+//   Eq. 3  d_i = MLP_decision(v_i): lane j < Hg computes hidden unit j (Hg <= 32 = warp)
+//   Eq. 4  M_i = 1 iff d_i > 0; CLS (token 0) is never reused
+//   HBM-bound: reads 2-3 fp32 rows of D per token.
+// compact_kernel (a4): Eq. 5-6 filtration as stream compaction (§5.3).
+//   One CTA per frame; the frame's output offset is the sum of |C| over earlier frames of the
+//   wave (integer, exact); a block-wide ballot scan ranks tokens.  Emits global rows
+//   slot*T + token, CLS first in each frame, tokens ascending: bit-exact, deterministic, and
+//   the counts never leave the device.
+#include "common.cuh"
+#include "rv_internal.h"
+
+namespace rv {
+namespace {
+
+constexpr int SCORE_THREADS = 256;
+
+__global__ void __launch_bounds__(SCORE_THREADS)
+    score_kernel(const float* __restrict__ X, int T, int D, int N, int L, int layer,
+                 const int4* __restrict__ wdesc, const float* __restrict__ tfeat,
+                 const float* __restrict__ codec, const uint8_t* force,
+                 const float* __restrict__ gate, int Hg, int dense, uint8_t* masks, float* scores,
+                 uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntC) {
+  __shared__ int s_reused;
+  const int w = blockIdx.x;
+  const int4 d4 = wdesc[w];
+  const int slot = d4.x, past = d4.y, fut = d4.z, type = d4.w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = SCORE_THREADS / 32;
+  if (threadIdx.x == 0) s_reused = 0;
+  const long long mrow = ((long long)slot * L + layer) * N;   // masks/scores row of (slot, layer)
+  const bool no_decision = dense || type == 0 || (past < 0 && fut < 0);
+  if (threadIdx.x == 0) {
+    wmask[(long long)w * T] = 0;
+    wprov[(long long)w * T] = 0;
+  }
+  if (no_decision) {
+    for (int i = 1 + threadIdx.x; i <= N; i += SCORE_THREADS) {
+      wmask[(long long)w * T + i] = 0;
+      wprov[(long long)w * T + i] = 0;
+      if (masks) masks[mrow + i - 1] = 0;
+      if (scores) scores[mrow + i - 1] = __int_as_float(0x7fc00000);   // NaN: no decision ran
+    }
+    if (threadIdx.x == 0) cntC[w] = T;
+    return;
+  }
+  __syncthreads();
+  // Decision-MLP weights of this layer: Wd1[7][Hg], bd1[Hg], Wd2[Hg], bd2[1].
+  float w1[7], b1 = 0.f, w2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) w1[k] = lane < Hg ? gate[k * Hg + lane] : 0.f;
+  if (lane < Hg) {
+    b1 = gate[7 * Hg + lane];
+    w2 = gate[8 * Hg + lane];
+  }
+  const float b2 = gate[9 * Hg];
+  const float oh0 = type == 0, oh1 = type == 1, oh2 = type == 2, oh3 = type == 3;
+  int my_reused = 0;
+  for (int i = 1 + warp; i <= N; i += nwarps) {
+    const float* cur = X + ((long long)slot * T + i) * D;
+    const float* rp = past >= 0 ? X + ((long long)past * T + i) * D : nullptr;
+    const float* rf = fut >= 0 ? X + ((long long)fut * T + i) * D : nullptr;
+    float cc = 0.f, pp = 0.f, ff = 0.f, cp = 0.f, cf = 0.f;
+    for (int k = lane; k < D; k += 32) {
+      const float c = cur[k];
+      cc += c * c;
+      if (rp) { const float p = rp[k]; pp += p * p; cp += c * p; }
+      if (rf) { const float f = rf[k]; ff += f * f; cf += c * f; }
+    }
+    cc = warp_sum(cc);
+    pp = warp_sum(pp);
+    ff = warp_sum(ff);
+    cp = warp_sum(cp);
+    cf = warp_sum(cf);
+    float s = -2.f;
+    int prov = 0;
+    if (rp) {
+      const float den = sqrtf(cc * pp);
+      s = den > 0.f ? cp / den : 0.f;
+    }
+    if (rf) {
+      const float den = sqrtf(cc * ff);
+      const float sf = den > 0.f ? cf / den : 0.f;
+      if (sf > s) { s = sf; prov = 1; }   // strict: ties keep the past reference
+    }
+    const float t = tfeat[(long long)slot * N + i - 1];
+    const float c = codec[(long long)slot * N + i - 1];
+    float h = b1 + s * w1[0] + t * w1[1] + oh0 * w1[2] + oh1 * w1[3] + oh2 * w1[4] + oh3 * w1[5] + c * w1[6];
+    h = lane < Hg ? quick_gelu(h) * w2 : 0.f;
+    const float dlogit = warp_sum(h) + b2;
+    int M = dlogit > 0.f ? 1 : 0;
+    if (force) M = force[mrow + i - 1] ? 1 : 0;
+    if (lane == 0) {
+      if (masks) masks[mrow + i - 1] = (uint8_t)M;
+      if (scores) scores[mrow + i - 1] = dlogit;
+      wmask[(long long)w * T + i] = (uint8_t)M;
+      wprov[(long long)w * T + i] = (uint8_t)prov;
+      my_reused += M;
+    }
+  }
+  if (lane == 0 && my_reused) atomicAdd(&s_reused, my_reused);
+  __syncthreads();
+  if (threadIdx.x == 0) cntC[w] = T - s_reused;
+}
+
+constexpr int COMPACT_THREADS = 256;
+
+__global__ void __launch_bounds__(COMPACT_THREADS)
+    compact_kernel(int n_w, int T, const int4* __restrict__ wdesc, const uint8_t* __restrict__ wmask,
+                   const uint8_t* __restrict__ wprov, const int* __restrict__ cntC, int* __restrict__ idxC,
+                   int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
+                   int* __restrict__ counts, unsigned long long* reuse_ctr) {
+  __shared__ int s_part[COMPACT_THREADS / 32];
+  __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
+  __shared__ int s_base[2];
+  const int w = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // offC = sum_{v<w} |C_v| (exact integer reduction)
+  int part = 0;
+  for (int v = threadIdx.x; v < w; v += COMPACT_THREADS) part += cntC[v];
+  part = warp_sum_i(part);
+  if (lane == 0) s_part[warp] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int k = 0; k < COMPACT_THREADS / 32; ++k) off += s_part[k];
+    s_base[0] = off;                 // C offset
+    s_base[1] = w * T - off;         // R offset (|R_v| = T - |C_v|)
+    qoff[w] = off;
+    if (w == n_w - 1) {
+      const int tot = off + cntC[w];
+      qoff[n_w] = tot;
+      counts[0] = tot;
+      counts[1] = n_w * T - tot;
+      if (reuse_ctr) atomicAdd(reuse_ctr, (unsigned long long)(n_w * T - tot));
+    }
+  }
+  __syncthreads();
+  const int4 d4 = wdesc[w];
+  const int slot = d4.x;
+  int offC = s_base[0], offR = s_base[1];
+  const uint8_t* mk = wmask + (long long)w * T;
+  const uint8_t* pv = wprov + (long long)w * T;
+  for (int base = 0; base < T; base += COMPACT_THREADS) {
+    const int i = base + threadIdx.x;
+    const bool valid = i < T;
+    const bool isC = valid && (i == 0 || mk[i] == 0);
+    const bool isR = valid && !isC;
+    const unsigned bc = __ballot_sync(0xffffffffu, isC);
+    const unsigned br = __ballot_sync(0xffffffffu, isR);
+    if (lane == 0) { s_wc[warp] = __popc(bc); s_wr[warp] = __popc(br); }
+    __syncthreads();
+    int pc = 0, pr = 0, tc = 0, tr = 0;
+    for (int k = 0; k < COMPACT_THREADS / 32; ++k) {
+      if (k < warp) { pc += s_wc[k]; pr += s_wr[k]; }
+      tc += s_wc[k];
+      tr += s_wr[k];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    if (isC) idxC[offC + pc + __popc(bc & lt)] = slot * T + i;
+    if (isR) {
+      const int r = offR + pr + __popc(br & lt);
+      idxR[r] = slot * T + i;
+      provrow[r] = (pv[i] ? d4.z : d4.y) * T + i;
+    }
+    offC += tc;
+    offR += tr;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
+                         const float* tfeat, const float* codec, const uint8_t* force, const float* gate,
+                         int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
+                         int* cntC, cudaStream_t s) {
+  if (n_w <= 0) return cudaSuccess;
+  score_kernel<<<n_w, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, reinterpret_cast<const int4*>(wdesc), tfeat,
+                                             codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntC);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
+                           const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
+                           unsigned long long* reuse_ctr, cudaStream_t s) {
+  if (n_w <= 0) return cudaSuccess;
+  compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
+                                                 cntC, idxC, idxR, provrow, qoff, counts, reuse_ctr);
+  return cudaGetLastError();
+}
+
+}  // namespace rv

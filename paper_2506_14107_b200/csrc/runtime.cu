@@ -1,0 +1,844 @@
+// runtime.cu — host runtime of libreusevit: the C-ABI (include/reusevit.h, reusevit_stages.h),
+// weight loading, the frame plan, the layer-wise / level-wave scheduler and the reuse cache.
+//
+// Scheduling (§5.1 P:492-501 layer-wise scheduling): for every layer l,
+// the dependency levels of the plan run one after another; each level is ONE compacted wave
+// over all resident frames of that level (SURVEY D8 generalises P:571-574's batching).  A
+// wave is: score (Eq. 1-4) -> compact (Eq. 5-6) -> gather+LN1 -> QKV GEMM (K/V scattered to
+// the cache) -> reused K/V copy + Delta (Eq. 8) -> attention -> CLS t -> W_o GEMM (+res) ->
+// LN2 -> FC1 GEMM (+QuickGELU) -> FC2 GEMM (+res, scatter, Eq. 10 C side) -> restoration
+// GEMMs (Eq. 9, scatter, Eq. 10 R side).  Counts stay on the device; the whole embed is
+// captured once into a CUDA graph and replayed ("avoiding frequent CPU-GPU
+// synchronization").
+//
+// Cached memory compaction (§5.2): the reuse cache holds only the current layer —
+// X ping-pong [2][n][T][D] fp32 and K/V [n][T][2D] bf16 — never every layer's activations.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/reusevit.h"
+#include "../../include/reusevit_stages.h"
+#include "rv_internal.h"
+
+using namespace rv;
+
+namespace {
+
+struct LayerW {
+  float *ln1_g, *ln1_b, *bqkv, *bo, *ln2_g, *ln2_b, *b1, *b2;
+  bf16 *Wqkv, *Wo, *W1, *W2;      // [out][in] bf16 (K-major B operands)
+  float* gate;                    // Wd1[7][Hg] | bd1[Hg] | Wd2[Hg] | bd2[1]  (fp32)
+  bf16 *Wr1, *Wr2;                // [Hr][D], [D][Hr] bf16
+  float *br1, *br2;
+};
+
+struct Wave {
+  int off;   // offset (in frames) into the concatenated wave descriptor array
+  int n_w;
+  bool any_ref;  // at least one frame with a decision (non-I, not dense)
+};
+
+thread_local std::string g_create_err;
+
+}  // namespace
+
+struct rv_ctx {
+  rv_config cfg{};
+  int L = 0, D = 0, H = 0, dh = 0, N = 0, T = 0, pp = 0, KP = 0, F = 0, Hr = 0, Hg = 0;
+  int device = 0;
+  std::string err;
+  // ---- weights (device)
+  std::vector<void*> wallocs;
+  bf16* W_pe = nullptr;
+  float *cls = nullptr, *pos = nullptr, *lnpre_g = nullptr, *lnpre_b = nullptr, *lnpost_g = nullptr,
+        *lnpost_b = nullptr;
+  std::vector<LayerW> lw;
+  bool vit_loaded = false, gates_loaded = false;
+  // ---- per-embed resources
+  int n_cap = 0;
+  long long capC = 0, capR = 0;   // row capacities of the wave buffers (multiples of 128)
+  std::vector<void*> ballocs;
+  float* X[2] = {nullptr, nullptr};
+  bf16* KV = nullptr;
+  float* pcls = nullptr;
+  bf16* patches_bf16 = nullptr;
+  float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
+  uint8_t* out_masks = nullptr;
+  int* wdesc = nullptr;
+  int wdesc_cap = 0;
+  uint8_t *wmask = nullptr, *wprov = nullptr;
+  int *cntC = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr;
+  bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *Ar = nullptr, *hr = nullptr;
+  float* x1 = nullptr;
+  unsigned long long* reuse_ctr = nullptr;   // [L]
+  // GEMM plans (tensor maps) bound to the buffers above
+  GemmPlan pe;
+  std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
+  // ---- graph cache
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<long long> gkey;
+  cudaStream_t own_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // ---- in-flight embed
+  bool inflight = false;
+  int cur_n = 0, cur_nonI = 0, cur_levels = 0, cur_launches = 0;
+  uint32_t cur_flags = 0;
+  cudaStream_t cur_stream = nullptr;
+  std::vector<Wave> waves;
+  std::vector<int> wdesc_host;
+};
+
+namespace {
+
+rv_status fail(rv_ctx* c, rv_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_create_err = buf;
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(ctx, RV_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+bool cfg_valid(const rv_config* c, char* why, size_t n) {
+  if (!c) { snprintf(why, n, "null config"); return false; }
+  if (c->layers < 1 || c->layers > 64) { snprintf(why, n, "layers must be 1..64"); return false; }
+  if (c->dim < 64 || c->dim > 1024 || c->dim % 64) { snprintf(why, n, "dim must be a multiple of 64 in [64,1024]"); return false; }
+  if (c->heads < 1 || c->dim % c->heads) { snprintf(why, n, "dim %% heads != 0 (S:99)"); return false; }
+  const int dh = c->dim / c->heads;
+  if (dh != 16 && dh != 64) { snprintf(why, n, "dim/heads must be 16 or 64"); return false; }
+  if (c->heads > 32) { snprintf(why, n, "heads must be <= 32"); return false; }
+  if (c->patch < 1 || c->img < c->patch || c->img % c->patch) { snprintf(why, n, "img must be a positive multiple of patch"); return false; }
+  const int N = (c->img / c->patch) * (c->img / c->patch);
+  if (N + 1 > 1024) { snprintf(why, n, "T = N+1 must be <= 1024"); return false; }
+  if (c->ffn < 64 || c->ffn % 64) { snprintf(why, n, "ffn must be a positive multiple of 64"); return false; }
+  if (c->hidden_r < 64 || c->hidden_r % 64) { snprintf(why, n, "hidden_r must be a positive multiple of 64"); return false; }
+  if (c->hidden_g < 1 || c->hidden_g > 32) { snprintf(why, n, "hidden_g must be 1..32"); return false; }
+  return true;
+}
+
+size_t vit_floats(const rv_config* c) {
+  const size_t D = c->dim, F = c->ffn, N = (size_t)(c->img / c->patch) * (c->img / c->patch), T = N + 1,
+               pp = 3ull * c->patch * c->patch;
+  size_t per = 2 * D + D * 3 * D + 3 * D + D * D + D + 2 * D + D * F + F + F * D + D;
+  return pp * D + D + T * D + 2 * D + c->layers * per + 2 * D;
+}
+size_t gate_floats(const rv_config* c) {
+  const size_t D = c->dim, Hr = c->hidden_r, Hg = c->hidden_g;
+  return c->layers * (7 * Hg + Hg + Hg + 1 + D * Hr + Hr + Hr * D + D);
+}
+
+template <class T>
+rv_status dalloc(rv_ctx* ctx, std::vector<void*>& list, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, RV_ENOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+  }
+  list.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return RV_OK;
+}
+
+// Host conversion helpers for weight upload.
+uint16_t f2bf(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  const uint32_t r = 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)((u + r) >> 16);
+}
+
+// Upload an [in][out] fp32 matrix as bf16 [out][inP] (transposed, K zero-padded to inP).
+rv_status upload_T(rv_ctx* ctx, std::vector<void*>& list, bf16** dst, const float* src, int in, int out, int inP) {
+  std::vector<uint16_t> tmp((size_t)out * inP, 0);
+  for (int i = 0; i < in; ++i)
+    for (int o = 0; o < out; ++o) tmp[(size_t)o * inP + i] = f2bf(src[(size_t)i * out + o]);
+  rv_status s = dalloc(ctx, list, dst, tmp.size());
+  if (s) return s;
+  CK(cudaMemcpy(*dst, tmp.data(), tmp.size() * 2, cudaMemcpyHostToDevice));
+  return RV_OK;
+}
+rv_status upload_f(rv_ctx* ctx, std::vector<void*>& list, float** dst, const float* src, size_t n) {
+  rv_status s = dalloc(ctx, list, dst, n);
+  if (s) return s;
+  CK(cudaMemcpy(*dst, src, n * 4, cudaMemcpyHostToDevice));
+  return RV_OK;
+}
+
+void free_list(std::vector<void*>& l) {
+  for (void* p : l) cudaFree(p);
+  l.clear();
+}
+
+// ------------------------------------------------------------------ plan helpers
+rv_status check_plan(rv_ctx* ctx, const rv_plan* p, std::vector<int>* level_out) {
+  if (!p || p->n < 1 || !p->type || !p->past || !p->future || !p->order)
+    return fail(ctx, RV_ECONTRACT, "plan: null array or n < 1");
+  const int n = p->n;
+  std::vector<int> pos(n, -1);
+  for (int k = 0; k < n; ++k) {
+    const int f = p->order[k];
+    if (f < 0 || f >= n || pos[f] >= 0) return fail(ctx, RV_EPLAN, "plan: order is not a permutation (at %d)", k);
+    pos[f] = k;
+  }
+  std::vector<int> lev(n, -1);
+  for (int k = 0; k < n; ++k) {
+    const int f = p->order[k];
+    const int t = p->type[f];
+    if (t < RV_I || t > RV_B1) return fail(ctx, RV_EPLAN, "plan: frame %d has bad type %d", f, t);
+    const int r[2] = {p->past[f], p->future[f]};
+    int lv = 0, nref = 0;
+    for (int j = 0; j < 2; ++j) {
+      if (r[j] == -1) continue;
+      if (r[j] < 0 || r[j] >= n || r[j] == f) return fail(ctx, RV_EPLAN, "plan: frame %d has bad reference %d", f, r[j]);
+      if (pos[r[j]] >= k) return fail(ctx, RV_EPLAN, "plan: frame %d references %d before it is computed (S:316)", f, r[j]);
+      lv = std::max(lv, lev[r[j]] + 1);
+      ++nref;
+    }
+    if (t == RV_I && nref) return fail(ctx, RV_EPLAN, "plan: I-frame %d has references", f);
+    if (t != RV_I && !nref) return fail(ctx, RV_EPLAN, "plan: non-I frame %d has no reference", f);
+    lev[f] = lv;
+  }
+  if (level_out) *level_out = lev;
+  return RV_OK;
+}
+
+// ------------------------------------------------------------------ buffers
+rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int max_w) {
+  capC = (capC + 127) / 128 * 128;
+  capR = std::max<long long>(128, (capR + 127) / 128 * 128);
+  if (n <= ctx->n_cap && capC <= ctx->capC && capR <= ctx->capR && max_w <= ctx->wdesc_cap) return RV_OK;
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  free_list(ctx->ballocs);
+  n = std::max(n, ctx->n_cap);
+  capC = std::max(capC, ctx->capC);
+  capR = std::max(capR, ctx->capR);
+  max_w = std::max(max_w, ctx->wdesc_cap);
+  const long long T = ctx->T, D = ctx->D, N = ctx->N;
+  auto& B = ctx->ballocs;
+  rv_status s;
+#define AL(ptr, cnt) if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) return s
+  AL(ctx->X[0], n * T * D);
+  AL(ctx->X[1], n * T * D);
+  AL(ctx->KV, n * T * 2 * D);
+  AL(ctx->pcls, n * N);
+  AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
+  AL(ctx->in_patches, (size_t)n * N * ctx->pp);
+  AL(ctx->in_codec, n * N);
+  AL(ctx->out_emb, n * D);
+  AL(ctx->out_masks, (size_t)n * ctx->L * N);
+  AL(ctx->out_scores, (size_t)n * ctx->L * N);
+  AL(ctx->wdesc, (size_t)n * 4);
+  AL(ctx->wmask, max_w * T);
+  AL(ctx->wprov, max_w * T);
+  AL(ctx->cntC, max_w);
+  AL(ctx->qoff, max_w + 1);
+  AL(ctx->counts, 2);
+  AL(ctx->idxC, capC);
+  AL(ctx->idxR, capR);
+  AL(ctx->provrow, capR);
+  AL(ctx->A, capC * D);
+  AL(ctx->q, capC * D);
+  AL(ctx->att, capC * D);
+  AL(ctx->x1, capC * D);
+  AL(ctx->h, capC * ctx->F);
+  AL(ctx->Ar, capR * D);
+  AL(ctx->hr, capR * ctx->Hr);
+  AL(ctx->reuse_ctr, 64);
+#undef AL
+  ctx->n_cap = n;
+  ctx->capC = capC;
+  ctx->capR = capR;
+  ctx->wdesc_cap = max_w;
+  char e[256];
+  if (!gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e))
+    return fail(ctx, RV_ECUDA, "%s", e);
+  const int L = ctx->L;
+  ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
+  ctx->g_r1.resize(L); ctx->g_r2.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = ctx->lw[l];
+    bool ok = gemm_make_plan(&ctx->g_qkv[l], ctx->A, capC, w.Wqkv, 3 * (int)D, (int)D, e, sizeof e) &&
+              gemm_make_plan(&ctx->g_wo[l], ctx->att, capC, w.Wo, (int)D, (int)D, e, sizeof e) &&
+              gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
+              gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e);
+    if (ok && ctx->gates_loaded)
+      ok = gemm_make_plan(&ctx->g_r1[l], ctx->Ar, capR, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
+           gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e);
+    if (!ok) return fail(ctx, RV_ECUDA, "%s", e);
+  }
+  return RV_OK;
+}
+
+// ------------------------------------------------------------------ the embed sequence
+struct Rec {
+  rv_ctx* ctx;
+  cudaStream_t s;
+  int launches = 0;
+  cudaError_t err = cudaSuccess;
+  const char* where = "";
+  void chk(cudaError_t e, const char* w) {
+    ++launches;
+    if (e != cudaSuccess && err == cudaSuccess) { err = e; where = w; }
+  }
+};
+
+void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patches, const float* codec,
+                  float* emb, uint8_t* masks, float* scores) {
+  const int L = ctx->L, D = ctx->D, T = ctx->T, N = ctx->N, H = ctx->H, F = ctx->F, Hr = ctx->Hr;
+  cudaStream_t s = r.s;
+  const bool dense = flags & RV_DENSE;
+  const bool force = flags & RV_FORCE_MASKS;
+  r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
+  --r.launches;
+  // a1: patch embed (dense, all frames): bf16 operand, GEMM into X0 rows f*T+1+i, finish.
+  r.chk(launch_patch_to_bf16(patches, ctx->patches_bf16, (long long)n * N, ctx->pp, ctx->KP, s), "patch_to_bf16");
+  {
+    Epi e;
+    e.out = ctx->X[0];
+    e.out_ld = D;
+    e.row_div = N;
+    e.row_add = 1;
+    r.chk(gemm_launch(ctx->pe, nullptr, n * N, n * N, e, s), "gemm_pe");
+  }
+  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pcls, n, T, D, N, s),
+        "embed_finish");
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = ctx->lw[l];
+    float* Xin = ctx->X[l & 1];
+    float* Xout = ctx->X[(l + 1) & 1];
+    for (const Wave& wv : ctx->waves) {
+      const int n_w = wv.n_w;
+      const int* wd = ctx->wdesc + (size_t)wv.off * 4;
+      const int maxC = n_w * T, maxR = n_w * N;
+      // a2-a3: Eq. 1-4
+      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pcls, codec, force ? masks : nullptr,
+                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
+                         ctx->wprov, ctx->cntC, s),
+            "score");
+      // a4: Eq. 5-6 stream compaction
+      r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntC, ctx->idxC, ctx->idxR, ctx->provrow,
+                           ctx->qoff, ctx->counts, ctx->reuse_ctr + l, s),
+            "compact");
+      const int* MC = ctx->counts;
+      const int* MR = ctx->counts + 1;
+      // a5: gather + LN1
+      r.chk(launch_gather_ln(Xin, ctx->idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, ctx->A, D, s), "gather_ln1");
+      // a6: QKV; q compact, K/V scattered to the cache rows of C
+      {
+        Epi e;
+        e.bias = w.bqkv;
+        e.out = ctx->q;
+        e.out_ld = D;
+        e.out_bf16 = 1;
+        e.split = D;
+        e.out2 = ctx->KV;
+        e.out2_rows = ctx->idxC;
+        e.out2_ld = 2LL * D;
+        e.out2_bf16 = 1;
+        r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
+      }
+      // a7 + Eq. 8: reused rows take the provider's K/V; Delta for the restoration layer
+      if (wv.any_ref) r.chk(launch_rgather(Xin, ctx->KV, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather");
+      // a8: attention over all T keys; CLS row -> t for layer l+1
+      r.chk(launch_attention(ctx->q, ctx->KV, ctx->att, wd, ctx->qoff, n_w, T, D, H, s), "attention");
+      if (!dense && l + 1 < L) r.chk(launch_cls_prob(ctx->q, ctx->KV, wd, ctx->qoff, ctx->pcls, n_w, T, D, H, s), "cls_prob");
+      // a9: W_o + residual (gathered X_{l-1} rows)
+      {
+        Epi e;
+        e.bias = w.bo;
+        e.resid = Xin;
+        e.resid_rows = ctx->idxC;
+        e.resid_ld = D;
+        e.out = ctx->x1;
+        e.out_ld = D;
+        r.chk(gemm_launch(ctx->g_wo[l], MC, 0, maxC, e, s), "gemm_wo");
+      }
+      // a10: LN2 + FC1 + QuickGELU
+      r.chk(launch_gather_ln(ctx->x1, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
+      {
+        Epi e;
+        e.bias = w.b1;
+        e.act = 1;
+        e.out = ctx->h;
+        e.out_ld = F;
+        e.out_bf16 = 1;
+        r.chk(gemm_launch(ctx->g_fc1[l], MC, 0, maxC, e, s), "gemm_fc1");
+      }
+      // a11: FC2 + residual, scattered to X_l rows of C (Eq. 10, C side)
+      {
+        Epi e;
+        e.bias = w.b2;
+        e.resid = ctx->x1;
+        e.resid_ld = D;
+        e.out = Xout;
+        e.out_rows = ctx->idxC;
+        e.out_ld = D;
+        r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
+      }
+      // a12: restoration (Eq. 9) + merge (Eq. 10, R side)
+      if (wv.any_ref) {
+        Epi e1;
+        e1.bias = w.br1;
+        e1.act = 1;
+        e1.out = ctx->hr;
+        e1.out_ld = Hr;
+        e1.out_bf16 = 1;
+        r.chk(gemm_launch(ctx->g_r1[l], MR, 0, maxR, e1, s), "gemm_r1");
+        Epi e2;
+        e2.bias = w.br2;
+        e2.resid = Xout;
+        e2.resid_rows = ctx->provrow;
+        e2.resid_ld = D;
+        e2.out = Xout;
+        e2.out_rows = ctx->idxR;
+        e2.out_ld = D;
+        r.chk(gemm_launch(ctx->g_r2[l], MR, 0, maxR, e2, s), "gemm_r2");
+      }
+    }
+  }
+  // a14: Z = LN_post(CLS), slots are display indices
+  r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* rv_status_string(rv_status s) {
+  switch (s) {
+    case RV_OK: return "RV_OK";
+    case RV_ECONFIG: return "RV_ECONFIG";
+    case RV_ESHAPE: return "RV_ESHAPE";
+    case RV_EPLAN: return "RV_EPLAN";
+    case RV_ECACHE: return "RV_ECACHE";
+    case RV_ECONTRACT: return "RV_ECONTRACT";
+    case RV_ECUDA: return "RV_ECUDA";
+    case RV_ENOMEM: return "RV_ENOMEM";
+    case RV_EBUSY: return "RV_EBUSY";
+  }
+  return "RV_UNKNOWN";
+}
+
+const char* rv_last_error(const rv_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+size_t rv_vit_blob_floats(const rv_config* cfg) {
+  char why[128];
+  return cfg_valid(cfg, why, sizeof why) ? vit_floats(cfg) : 0;
+}
+size_t rv_gate_blob_floats(const rv_config* cfg) {
+  char why[128];
+  return cfg_valid(cfg, why, sizeof why) ? gate_floats(cfg) : 0;
+}
+
+rv_status rv_plan_gop(int32_t n, int32_t refresh, int32_t reorder, rv_plan* out) {
+  rv_ctx* ctx = nullptr;
+  if (!out || !out->type || !out->past || !out->future || !out->order) return fail(ctx, RV_ECONTRACT, "rv_plan_gop: null output");
+  if (n < 1) return fail(ctx, RV_ECONFIG, "rv_plan_gop: n must be >= 1");
+  if (refresh < 4 || refresh % 4) return fail(ctx, RV_ECONFIG, "rv_plan_gop: refresh must be a multiple of 4 (S:310)");
+  out->n = n;
+  for (int i = 0; i < n; ++i) { out->type[i] = RV_I; out->past[i] = -1; out->future[i] = -1; }
+  int k = 0;
+  if (!reorder) {   // low-latency mode: each frame references its predecessor
+    for (int i = 0; i < n; ++i) {
+      if (i % refresh) { out->type[i] = RV_P; out->past[i] = i - 1; }
+      out->order[k++] = i;
+    }
+    return RV_OK;
+  }
+  out->order[k++] = 0;   // I
+  for (int a0 = 0; a0 + 1 < n; a0 += 4) {   // 5-frame unit [a0 .. a0+4]
+    const int a1 = a0 + 4;
+    if (a1 < n) {
+      if (a1 % refresh) { out->type[a1] = RV_P; out->past[a1] = a0; }
+      out->order[k++] = a1;
+    }
+    if (a0 + 2 < n) {
+      out->type[a0 + 2] = RV_B2;
+      out->past[a0 + 2] = a0;
+      out->future[a0 + 2] = a1 < n ? a1 : -1;
+      out->order[k++] = a0 + 2;
+    }
+    for (int b : {a0 + 1, a0 + 3}) {
+      if (b < n) {
+        out->type[b] = RV_B1;
+        out->past[b] = b - 1;
+        out->future[b] = b + 1 < n ? b + 1 : -1;
+        out->order[k++] = b;
+      }
+    }
+  }
+  return RV_OK;
+}
+
+rv_status rv_plan_check(const rv_plan* plan) { return check_plan(nullptr, plan, nullptr); }
+
+rv_status rv_create(const rv_config* cfg, int device, rv_ctx** out) {
+  rv_ctx* ctx = nullptr;
+  if (!out) return fail(ctx, RV_ECONTRACT, "rv_create: out is NULL");
+  *out = nullptr;
+  char why[160];
+  if (!cfg_valid(cfg, why, sizeof why)) return fail(ctx, RV_ECONFIG, "rv_create: %s", why);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(ctx, RV_ECUDA, "rv_create: no CUDA device (%s); there is no CPU fallback",
+                e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  }
+  if (device < 0 || device >= ndev) return fail(ctx, RV_ECUDA, "rv_create: device %d out of range (%d)", device, ndev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+    return fail(ctx, RV_ECUDA, "rv_create: device %d is sm_%d%d; this library is built for sm_100a only", device,
+                prop.major, prop.minor);
+  if (cudaSetDevice(device) != cudaSuccess) return fail(ctx, RV_ECUDA, "rv_create: cudaSetDevice failed");
+  ctx = new rv_ctx();
+  ctx->cfg = *cfg;
+  ctx->device = device;
+  ctx->L = cfg->layers;
+  ctx->D = cfg->dim;
+  ctx->H = cfg->heads;
+  ctx->dh = cfg->dim / cfg->heads;
+  ctx->N = (cfg->img / cfg->patch) * (cfg->img / cfg->patch);
+  ctx->T = ctx->N + 1;
+  ctx->pp = 3 * cfg->patch * cfg->patch;
+  ctx->KP = (ctx->pp + 63) / 64 * 64;
+  ctx->F = cfg->ffn;
+  ctx->Hr = cfg->hidden_r;
+  ctx->Hg = cfg->hidden_g;
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  *out = ctx;
+  return RV_OK;
+}
+
+rv_status rv_load_vit(rv_ctx* ctx, const float* blob, size_t n_floats) {
+  if (!ctx) return RV_ECONTRACT;
+  if (!blob) return fail(ctx, RV_ECONTRACT, "rv_load_vit: blob is NULL");
+  if (ctx->inflight) return fail(ctx, RV_EBUSY, "rv_load_vit: embed in flight");
+  const size_t want = vit_floats(&ctx->cfg);
+  if (n_floats != want) return fail(ctx, RV_ESHAPE, "rv_load_vit: blob has %zu floats, config needs %zu", n_floats, want);
+  CK(cudaSetDevice(ctx->device));
+  const int D = ctx->D, T = ctx->T, F = ctx->F, pp = ctx->pp;
+  // weights of a previous load stay allocated until destroy (gates share the list)
+  std::vector<void*>& W = ctx->wallocs;
+  const float* p = blob;
+  rv_status s;
+  if ((s = upload_T(ctx, W, &ctx->W_pe, p, pp, D, ctx->KP))) return s;
+  p += (size_t)pp * D;
+  if ((s = upload_f(ctx, W, &ctx->cls, p, D))) return s;
+  p += D;
+  if ((s = upload_f(ctx, W, &ctx->pos, p, (size_t)T * D))) return s;
+  p += (size_t)T * D;
+  if ((s = upload_f(ctx, W, &ctx->lnpre_g, p, D))) return s;
+  p += D;
+  if ((s = upload_f(ctx, W, &ctx->lnpre_b, p, D))) return s;
+  p += D;
+  ctx->lw.resize(ctx->L);
+  for (int l = 0; l < ctx->L; ++l) {
+    LayerW& w = ctx->lw[l];
+    if ((s = upload_f(ctx, W, &w.ln1_g, p, D))) return s; p += D;
+    if ((s = upload_f(ctx, W, &w.ln1_b, p, D))) return s; p += D;
+    if ((s = upload_T(ctx, W, &w.Wqkv, p, D, 3 * D, D))) return s; p += (size_t)D * 3 * D;
+    if ((s = upload_f(ctx, W, &w.bqkv, p, 3 * D))) return s; p += 3 * D;
+    if ((s = upload_T(ctx, W, &w.Wo, p, D, D, D))) return s; p += (size_t)D * D;
+    if ((s = upload_f(ctx, W, &w.bo, p, D))) return s; p += D;
+    if ((s = upload_f(ctx, W, &w.ln2_g, p, D))) return s; p += D;
+    if ((s = upload_f(ctx, W, &w.ln2_b, p, D))) return s; p += D;
+    if ((s = upload_T(ctx, W, &w.W1, p, D, F, D))) return s; p += (size_t)D * F;
+    if ((s = upload_f(ctx, W, &w.b1, p, F))) return s; p += F;
+    if ((s = upload_T(ctx, W, &w.W2, p, F, D, F))) return s; p += (size_t)F * D;
+    if ((s = upload_f(ctx, W, &w.b2, p, D))) return s; p += D;
+  }
+  if ((s = upload_f(ctx, W, &ctx->lnpost_g, p, D))) return s;
+  p += D;
+  if ((s = upload_f(ctx, W, &ctx->lnpost_b, p, D))) return s;
+  p += D;
+  ctx->vit_loaded = true;
+  ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0;   // re-encode tensor maps
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  return RV_OK;
+}
+
+rv_status rv_load_gates(rv_ctx* ctx, const float* blob, size_t n_floats) {
+  if (!ctx) return RV_ECONTRACT;
+  if (!blob) return fail(ctx, RV_ECONTRACT, "rv_load_gates: blob is NULL");
+  if (!ctx->vit_loaded) return fail(ctx, RV_ECONTRACT, "rv_load_gates: load the ViT weights first");
+  if (ctx->inflight) return fail(ctx, RV_EBUSY, "rv_load_gates: embed in flight");
+  const size_t want = gate_floats(&ctx->cfg);
+  if (n_floats != want) return fail(ctx, RV_ESHAPE, "rv_load_gates: blob has %zu floats, config needs %zu", n_floats, want);
+  CK(cudaSetDevice(ctx->device));
+  const int D = ctx->D, Hr = ctx->Hr, Hg = ctx->Hg;
+  std::vector<void*>& W = ctx->wallocs;
+  const float* p = blob;
+  rv_status s;
+  for (int l = 0; l < ctx->L; ++l) {
+    LayerW& w = ctx->lw[l];
+    const size_t ng = 7 * Hg + Hg + Hg + 1;
+    if ((s = upload_f(ctx, W, &w.gate, p, ng))) return s; p += ng;
+    if ((s = upload_T(ctx, W, &w.Wr1, p, D, Hr, D))) return s; p += (size_t)D * Hr;
+    if ((s = upload_f(ctx, W, &w.br1, p, Hr))) return s; p += Hr;
+    if ((s = upload_T(ctx, W, &w.Wr2, p, Hr, D, Hr))) return s; p += (size_t)Hr * D;
+    if ((s = upload_f(ctx, W, &w.br2, p, D))) return s; p += D;
+  }
+  ctx->gates_loaded = true;
+  ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0;
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  return RV_OK;
+}
+
+rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const rv_plan* plan, uint32_t flags,
+                   void* cuda_stream, float* emb, uint8_t* masks, float* scores) {
+  if (!ctx) return RV_ECONTRACT;
+  if (ctx->inflight) return fail(ctx, RV_EBUSY, "rv_embed: an embed is already in flight");
+  if (!ctx->vit_loaded) return fail(ctx, RV_ECONTRACT, "rv_embed: ViT weights not loaded");
+  const bool dense = flags & RV_DENSE;
+  if (!dense && !ctx->gates_loaded) return fail(ctx, RV_ECONTRACT, "rv_embed: gates not loaded (or pass RV_DENSE)");
+  if (!patches || !codec || !emb) return fail(ctx, RV_ECONTRACT, "rv_embed: patches, codec and emb are required");
+  if ((flags & RV_FORCE_MASKS) && !masks) return fail(ctx, RV_ECONTRACT, "rv_embed: RV_FORCE_MASKS needs masks");
+  std::vector<int> lev;
+  rv_status st = check_plan(ctx, plan, &lev);
+  if (st) return st;
+  CK(cudaSetDevice(ctx->device));
+  const int n = plan->n, T = ctx->T, N = ctx->N, L = ctx->L, D = ctx->D;
+  // ---- level-waves: frames of equal level in computation order; dense = one level.
+  // Large levels are split into waves of at most kMaxWave frames (bounds the wave buffers).
+  const int kMaxWave = 1536;
+  std::vector<std::vector<int>> levels;
+  for (int k = 0; k < n; ++k) {
+    const int f = plan->order[k];
+    const int lv = dense ? 0 : lev[f];
+    if ((int)levels.size() <= lv) levels.resize(lv + 1);
+    levels[lv].push_back(f);
+  }
+  ctx->waves.clear();
+  ctx->wdesc_host.clear();
+  int max_w = 0, nonI = 0;
+  bool any_ref_all = false;
+  for (auto& lvf : levels) {
+    for (size_t b = 0; b < lvf.size(); b += kMaxWave) {
+      Wave wv;
+      wv.off = (int)ctx->wdesc_host.size() / 4;
+      wv.n_w = (int)std::min<size_t>(kMaxWave, lvf.size() - b);
+      wv.any_ref = false;
+      for (int j = 0; j < wv.n_w; ++j) {
+        const int f = lvf[b + j];
+        const int t = dense ? RV_I : plan->type[f];
+        ctx->wdesc_host.push_back(f);
+        ctx->wdesc_host.push_back(dense ? -1 : plan->past[f]);
+        ctx->wdesc_host.push_back(dense ? -1 : plan->future[f]);
+        ctx->wdesc_host.push_back(t);
+        if (t != RV_I) { wv.any_ref = true; }
+      }
+      any_ref_all |= wv.any_ref;
+      max_w = std::max(max_w, wv.n_w);
+      ctx->waves.push_back(wv);
+    }
+  }
+  for (int f = 0; f < n; ++f) nonI += (!dense && plan->type[f] != RV_I);
+  const int total_desc = (int)ctx->wdesc_host.size() / 4;
+  if (total_desc != n) return fail(ctx, RV_EPLAN, "rv_embed: internal wave bookkeeping mismatch");
+  if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w)))
+    return st;
+  cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : nullptr;
+  const bool devp = flags & RV_DEVICE_PTRS;
+  const float* d_patches = devp ? patches : ctx->in_patches;
+  const float* d_codec = devp ? codec : ctx->in_codec;
+  float* d_emb = devp ? emb : ctx->out_emb;
+  uint8_t* d_masks = devp ? (masks ? masks : ctx->out_masks) : ctx->out_masks;
+  float* d_scores = devp ? (scores ? scores : ctx->out_scores) : ctx->out_scores;
+  // Graph capture cannot run on the legacy NULL stream: work on the context's own stream,
+  // ordered after / before the caller's stream with events.
+  cudaStream_t ws = s ? s : ctx->own_stream;
+  if (!s) {
+    CK(cudaEventRecord(ctx->ev[3], 0));
+    CK(cudaStreamWaitEvent(ws, ctx->ev[3], 0));
+  }
+  CK(cudaEventRecord(ctx->ev[0], ws));
+  CK(cudaMemcpyAsync(ctx->wdesc, ctx->wdesc_host.data(), ctx->wdesc_host.size() * sizeof(int),
+                     cudaMemcpyHostToDevice, ws));
+  if (!devp) {
+    CK(cudaMemcpyAsync(ctx->in_patches, patches, (size_t)n * N * ctx->pp * 4, cudaMemcpyHostToDevice, ws));
+    CK(cudaMemcpyAsync(ctx->in_codec, codec, (size_t)n * N * 4, cudaMemcpyHostToDevice, ws));
+    if (flags & RV_FORCE_MASKS)
+      CK(cudaMemcpyAsync(ctx->out_masks, masks, (size_t)n * L * N, cudaMemcpyHostToDevice, ws));
+  }
+  CK(cudaEventRecord(ctx->ev[1], ws));
+  // ---- compute: cached CUDA graph keyed on everything the recorded sequence depends on
+  std::vector<long long> key = {(long long)n, (long long)(flags & ~RV_NO_GRAPH), (long long)(intptr_t)d_patches,
+                                (long long)(intptr_t)d_codec, (long long)(intptr_t)d_emb,
+                                (long long)(intptr_t)d_masks, (long long)(intptr_t)d_scores,
+                                (long long)(intptr_t)ws, ctx->capC, ctx->capR};
+  for (int v : ctx->wdesc_host) key.push_back(v);
+  Rec rec{ctx, ws};
+  if (flags & RV_NO_GRAPH) {
+    record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
+    if (rec.err != cudaSuccess) return fail(ctx, RV_ECUDA, "launch %s: %s", rec.where, cudaGetErrorString(rec.err));
+  } else {
+    if (!ctx->gexec || key != ctx->gkey) {
+      if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
+      record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
+      cudaError_t ce = cudaStreamEndCapture(ws, &g);
+      if (rec.err != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return fail(ctx, RV_ECUDA, "capture %s: %s", rec.where, cudaGetErrorString(rec.err));
+      }
+      CK(ce);
+      cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      ctx->gkey = key;
+      ctx->cur_launches = rec.launches;
+    }
+    CK(cudaGraphLaunch(ctx->gexec, ws));
+    rec.launches = ctx->cur_launches;
+  }
+  CK(cudaEventRecord(ctx->ev[2], ws));
+  if (!devp) {
+    CK(cudaMemcpyAsync(emb, ctx->out_emb, (size_t)n * D * 4, cudaMemcpyDeviceToHost, ws));
+    if (masks && !(flags & RV_FORCE_MASKS))
+      CK(cudaMemcpyAsync(masks, ctx->out_masks, (size_t)n * L * N, cudaMemcpyDeviceToHost, ws));
+    if (scores) CK(cudaMemcpyAsync(scores, ctx->out_scores, (size_t)n * L * N * 4, cudaMemcpyDeviceToHost, ws));
+  }
+  CK(cudaEventRecord(ctx->ev[3], ws));
+  if (!s) CK(cudaStreamWaitEvent(0, ctx->ev[3], 0));
+  ctx->inflight = true;
+  ctx->cur_n = n;
+  ctx->cur_nonI = nonI;
+  ctx->cur_flags = flags;
+  ctx->cur_levels = (int)levels.size();
+  ctx->cur_launches = rec.launches;
+  ctx->cur_stream = ws;
+  return RV_OK;
+}
+
+rv_status rv_wait(rv_ctx* ctx, rv_stats* stats) {
+  if (!ctx) return RV_ECONTRACT;
+  if (!ctx->inflight) return fail(ctx, RV_ECONTRACT, "rv_wait: no embed in flight");
+  ctx->inflight = false;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventSynchronize(ctx->ev[3]));
+  CK(cudaGetLastError());
+  if (!stats) return RV_OK;
+  memset(stats, 0, sizeof *stats);
+  const int L = ctx->L, n = ctx->cur_n, T = ctx->T, N = ctx->N;
+  unsigned long long ctr[64] = {0};
+  CK(cudaMemcpy(ctr, ctx->reuse_ctr, L * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  const double D = ctx->D, F = ctx->F, Hr = ctx->Hr, pp = ctx->pp;
+  const double per_c = 2 * D * 3 * D + 2 * D * D + 4 * D * F + 4 * T * D;
+  const double per_r = 4 * D * Hr;
+  double reused = 0, flops = 2.0 * n * N * pp * D, bytes = 0;
+  for (int l = 0; l < L; ++l) {
+    const double r = (double)ctr[l];
+    const double c = (double)n * T - r;
+    reused += r;
+    flops += c * per_c + r * per_r;
+    // algorithmic bytes: 60 D per recomputed token-layer, 18 D per reused one
+    bytes += c * 60.0 * D + r * 18.0 * D;
+    stats->reuse_by_layer[l] = ctx->cur_nonI ? (float)(r / ((double)ctx->cur_nonI * N)) : 0.f;
+  }
+  stats->reuse_nonI = ctx->cur_nonI ? reused / ((double)ctx->cur_nonI * L * N) : 0.0;
+  stats->reuse_all = reused / ((double)n * L * T);
+  stats->flops_exec = flops;
+  stats->flops_dense = 2.0 * n * N * pp * D + (double)n * L * T * per_c;
+  stats->bytes_alg = bytes;
+  const double cache = (double)n * T * (2 * D * 4 + 2 * D * 2);
+  stats->peak_cache_bytes = (uint64_t)cache;
+  stats->keepall_cache_bytes = (uint64_t)((double)n * T * ((L + 1) * D * 4 + L * 2 * D * 2));
+  float ms = 0, msc = 0;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
+  cudaEventElapsedTime(&msc, ctx->ev[1], ctx->ev[2]);
+  stats->ms_total = ms;
+  stats->ms_compute = msc;
+  stats->n_levels = ctx->cur_levels;
+  stats->n_launches = ctx->cur_launches;
+  return RV_OK;
+}
+
+void rv_destroy(rv_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->inflight) cudaEventSynchronize(ctx->ev[3]);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  free_list(ctx->ballocs);
+  free_list(ctx->wallocs);
+  for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+// ---------------------------------------------------------------------- stage entry points
+rv_status rv_stage_score(rv_ctx* ctx, int32_t layer, const float* X, int32_t n_w, const int32_t* wdesc,
+                         const float* t, const float* codec, const uint8_t* force, uint8_t* masks, float* scores,
+                         uint8_t* wmask, uint8_t* wprov, int32_t* cntC, void* stream) {
+  if (!ctx) return RV_ECONTRACT;
+  if (!ctx->gates_loaded) return fail(ctx, RV_ECONTRACT, "rv_stage_score: gates not loaded");
+  if (layer < 0 || layer >= ctx->L || n_w < 0) return fail(ctx, RV_ECONTRACT, "rv_stage_score: bad layer/n_w");
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_score(X, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, codec, force, ctx->lw[layer].gate,
+                  ctx->Hg, 0, masks, scores, wmask, wprov, cntC, (cudaStream_t)stream));
+  return RV_OK;
+}
+
+rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const uint8_t* wmask,
+                           const uint8_t* wprov, const int32_t* cntC, int32_t* idxC, int32_t* idxR,
+                           int32_t* provrow, int32_t* qoff, int32_t* counts, void* stream) {
+  if (!ctx) return RV_ECONTRACT;
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntC, idxC, idxR, provrow, qoff, counts, nullptr,
+                    (cudaStream_t)stream));
+  return RV_OK;
+}
+
+rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void* A, const void* B, const float* bias,
+                        int32_t act, void* out, int32_t out_bf16, void* stream) {
+  if (!ctx) return RV_ECONTRACT;
+  if (M < 0 || N % 64 || K % 64 || N <= 0 || K <= 0 || !A || !B || !out)
+    return fail(ctx, RV_ECONTRACT, "rv_stage_gemm: need M >= 0, N and K positive multiples of 64");
+  CK(cudaSetDevice(ctx->device));
+  GemmPlan p;
+  char e[256];
+  if (!gemm_make_plan(&p, A, std::max(M, 1), B, N, K, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+  Epi ep;
+  ep.bias = bias;
+  ep.act = act;
+  ep.out = out;
+  ep.out_ld = N;
+  ep.out_bf16 = out_bf16;
+  CK(gemm_launch(p, nullptr, M, M, ep, (cudaStream_t)stream));
+  return RV_OK;
+}
+
+rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const int32_t* qoff, const void* q,
+                             const void* KV, void* out, float* pcls, void* stream) {
+  if (!ctx) return RV_ECONTRACT;
+  CK(cudaSetDevice(ctx->device));
+  CK(launch_attention((const bf16*)q, (const bf16*)KV, (bf16*)out, wdesc, qoff, n_w, ctx->T, ctx->D, ctx->H,
+                      (cudaStream_t)stream));
+  if (pcls)
+    CK(launch_cls_prob((const bf16*)q, (const bf16*)KV, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
+                       (cudaStream_t)stream));
+  return RV_OK;
+}
+
+}  // extern "C"

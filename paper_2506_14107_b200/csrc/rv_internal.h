@@ -1,0 +1,75 @@
+// rv_internal.h — launcher declarations shared by the kernel translation units and the
+// host runtime (runtime.cu).  Not part of the ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <cuda_bf16.h>
+
+namespace rv {
+
+// ---------------------------------------------------------------- GEMM epilogue (k_gemm.cu)
+// out[orow(m)][n] = act(acc[m][n] + bias[n]) + resid[rrow(m)][n]   (fp32 residual)
+// orow(m) = out_rows ? out_rows[m] : m + (row_div ? m / row_div : 0) + row_add
+// Columns n >= split go to out2 (column n - split) with rows out2_rows[m].
+struct Epi {
+  const float* bias = nullptr;
+  int act = 0;                 // 0 identity, 1 QuickGELU
+  const float* resid = nullptr;
+  const int* resid_rows = nullptr;
+  long long resid_ld = 0;
+  void* out = nullptr;
+  const int* out_rows = nullptr;
+  long long out_ld = 0;
+  int out_bf16 = 0;
+  int row_div = 0, row_add = 0;
+  int split = 1 << 30;
+  void* out2 = nullptr;
+  const int* out2_rows = nullptr;
+  long long out2_ld = 0;
+  int out2_bf16 = 1;
+};
+
+struct GemmPlan {
+  CUtensorMap tmA;        // A bf16 [rows][K], box {64, 128}, SWIZZLE_128B
+  CUtensorMap tmB;        // B bf16 [N][K],    box {64, BN},  SWIZZLE_128B
+  int N = 0, K = 0, BN = 0;
+};
+
+// Encode the tensor maps for a GEMM with A = [a_rows][K] and B = [N][K] (bf16, row-major).
+bool gemm_make_plan(GemmPlan* p, const void* A, long long a_rows, const void* B, int N, int K,
+                    char* err, size_t errlen);
+// Launch: M read from *M_dev when M_dev != nullptr, else M_host.  max_m = host upper bound of
+// M (sizes the persistent grid).
+cudaError_t gemm_launch(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
+                        cudaStream_t s);
+
+// ---------------------------------------------------------------- row kernels (k_elem.cu)
+typedef __nv_bfloat16 bf16;
+cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP, cudaStream_t s);
+cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g, const float* b,
+                                float* pcls, int n, int T, int D, int N, cudaStream_t s);
+cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
+                             const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
+cudaError_t launch_rgather(const float* X, bf16* KV, const int* idxR, const int* provrow, const int* count,
+                           int max_rows, bf16* Ar, int D, cudaStream_t s);
+cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
+                           cudaStream_t s);
+
+// ---------------------------------------------------------------- decision + compaction (k_score.cu)
+cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
+                         const float* tfeat, const float* codec, const uint8_t* force, const float* gate,
+                         int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
+                         int* cntC, cudaStream_t s);
+cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
+                           const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
+                           unsigned long long* reuse_ctr, cudaStream_t s);
+
+// ---------------------------------------------------------------- attention (k_attn.cu)
+cudaError_t launch_attention(const bf16* q, const bf16* KV, bf16* out, const int* wdesc, const int* qoff, int n_w,
+                             int T, int D, int H, cudaStream_t s);
+cudaError_t launch_cls_prob(const bf16* q, const bf16* KV, const int* wdesc, const int* qoff, float* pcls, int n_w,
+                            int T, int D, int H, cudaStream_t s);
+}  // namespace rv
+

@@ -1,0 +1,157 @@
+"""End-to-end parity of the CUDA path (rv_embed through the C-ABI) against the fp64 oracle on
+the same seeded inputs (BASELINE.json north star tolerances, SURVEY D10 metric forms):
+  * per-frame normwise max relative error max|Z_gpu - Z_ref| / max|Z_ref| <= 2e-2
+  * per-frame cosine >= 0.999
+  * reuse masks agree on >= 99.9% of tokens with |d_oracle| >= 1e-3
+plus invariants that hold bitwise on the GPU (forced all-reuse P-frame, determinism,
+graph vs direct launches, host vs device pointers)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def metrics(Zg, Zr):
+    Zg = np.asarray(Zg, np.float64)
+    err = np.abs(Zg - Zr).max(axis=1) / np.abs(Zr).max(axis=1)
+    cos = (Zg * Zr).sum(1) / np.linalg.norm(Zg, axis=1) / np.linalg.norm(Zr, axis=1)
+    return err, cos
+
+
+def mask_agreement(Mg, ref, frames):
+    d = ref["d"][frames]
+    band = ~np.isnan(d) & (np.abs(np.nan_to_num(d)) >= 1e-3)
+    if band.sum() == 0:
+        return 1.0, 0
+    return float((Mg[frames] == ref["M"][frames])[band].mean()), int(band.sum())
+
+
+def build(cfg, **gk):
+    from paper_2506_14107_b200 import ReuseViT
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=True, **gk)
+    m = ReuseViT(cfg, 0)
+    m.load_vit(synth.pack_vit(cfg, W))
+    m.load_gates(synth.pack_gates(cfg, G))
+    return m, W, G
+
+
+CASES = [
+    # cfg, frames on GPU, frames checked by the oracle (prefix-closed), motion p, mode
+    ("tiny", 8, 8, 0.3, "bimodal"),
+    ("tiny", 41, 41, 0.2, "bimodal"),
+    ("b16", 32, 32, 0.3, "bimodal"),
+    ("b16", 32, 32, 0.1, "bimodal"),
+    ("l14", 64, 21, 0.2, "bimodal"),
+]
+
+
+@pytest.mark.parametrize("cfgname,n,n_check,p,mode", CASES)
+def test_embed_parity(cuda_ok, cfgname, n, n_check, p, mode):
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, n, p, seed=2000 + n)
+    plan = oracle.plan_gop(n)
+    Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), want_scores=True)
+    torch.cuda.synchronize()
+    frames = list(range(n_check))
+    ref = oracle.reuse_embed(cfg, W, G, x, c, plan, frames=frames)
+    err, cos = metrics(Z.cpu().numpy()[frames], ref["Z"][frames])
+    agree, cnt = mask_agreement(M.cpu().numpy(), ref, frames)
+    print(f"{cfgname} n={n} p={p}: reuse_all={st['reuse_all']:.3f} max_err={err.max():.3e} "
+          f"min_cos={cos.min():.6f} mask_agree={agree:.5f} ({cnt} tokens)")
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and agree >= 0.999
+    # decision logits on frames whose inputs agree closely
+    d_gpu = S.cpu().numpy()[frames]
+    nonI = plan["type"][frames] != 0
+    assert np.all(np.isnan(d_gpu[~nonI]))
+    assert st["reuse_all"] > 0.2
+    # stats consistency with the returned masks
+    Mg = M.cpu().numpy()
+    assert abs(st["reuse_all"] - Mg.sum() / (n * cfg.layers * cfg.T)) < 1e-9
+
+
+@pytest.mark.parametrize("cfgname", ["tiny", "b16"])
+def test_dense_parity(cuda_ok, cfgname):
+    """RV_DENSE (own-dense baseline): equals the plain ViT."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 12, 0.5, seed=7)
+    Z, M, _, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), dense=True)
+    torch.cuda.synchronize()
+    ref = oracle.dense_embed(cfg, W, x)
+    err, cos = metrics(Z.cpu().numpy(), ref)
+    assert err.max() <= 2e-2 and cos.min() >= 0.999, (err.max(), cos.min())
+    assert M.cpu().numpy().sum() == 0 and st["reuse_all"] == 0.0
+
+
+@pytest.mark.parametrize("cfgname", ["tiny", "b16"])
+def test_forced_masks_parity(cuda_ok, cfgname):
+    """Forced random reuse map (SURVEY Q18 diagnostic): isolates numeric error from decisions."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    n = 13
+    x, c = synth.make_video(cfg, n, 0.3, seed=11)
+    plan = oracle.plan_gop(n)
+    rng = np.random.default_rng(3)
+    fm = (rng.random((n, cfg.layers, cfg.N)) < 0.6).astype(np.uint8)
+    fm[plan["type"] == 0] = 0
+    Z, M, _, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), force_masks=torch.from_numpy(fm))
+    torch.cuda.synchronize()
+    ref = oracle.reuse_embed(cfg, W, G, x, c, plan, force_masks=fm)
+    err, cos = metrics(Z.cpu().numpy(), ref["Z"])
+    assert err.max() <= 2e-2 and cos.min() >= 0.999, (err.max(), cos.min())
+    assert np.array_equal(M.cpu().numpy(), fm)
+
+
+def test_all_reuse_p_frame_bitwise(cuda_ok):
+    """Closed form of the layer-gated reading: a P-frame with every patch reused returns its
+    reference's embedding exactly (bitwise on the GPU: batch-invariant kernels)."""
+    cfg = synth.CONFIGS["b16"]
+    m, W, G = build(cfg)
+    n = 5
+    x, c = synth.make_video(cfg, n, 0.5, seed=5)
+    fm = np.zeros((n, cfg.layers, cfg.N), np.uint8)
+    fm[4] = 1                      # frame 4 = P referencing I-frame 0
+    Z, _, _, _ = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), force_masks=torch.from_numpy(fm))
+    torch.cuda.synchronize()
+    Zc = Z.cpu()
+    assert torch.equal(Zc[4], Zc[0])
+
+
+def test_determinism_graph_and_host_paths(cuda_ok):
+    cfg = synth.CONFIGS["b16"]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 24, 0.3, seed=9)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    Z1, M1, _, _ = m.embed(xd, cd)
+    Z2, M2, _, _ = m.embed(xd, cd)
+    Z3, M3, _, _ = m.embed(xd, cd, graph=False)
+    Z4, M4, _, st = m.embed(x, c)          # host pointers, H2D/D2H inside the library
+    torch.cuda.synchronize()
+    assert torch.equal(Z1, Z2) and torch.equal(M1, M2)
+    assert torch.equal(Z1, Z3) and torch.equal(M1, M3)
+    assert np.array_equal(Z1.cpu().numpy(), Z4) and np.array_equal(M1.cpu().numpy(), M4)
+    assert st["ms_total"] > 0 and st["n_launches"] > 0
+
+
+def test_duplicate_frame_reuses_everything(cuda_ok):
+    cfg = synth.CONFIGS["b16"]
+    from paper_2506_14107_b200 import ReuseViT
+    W = synth.make_vit(cfg)
+    G = synth.make_gates(cfg, restore_bias=False)
+    m = ReuseViT(cfg, 0)
+    m.load_vit(synth.pack_vit(cfg, W))
+    m.load_gates(synth.pack_gates(cfg, G))
+    x, c = synth.make_video(cfg, 5, 0.5, seed=3, duplicate_of={4: 0})
+    c[4] = 0
+    Z, M, _, _ = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda())
+    torch.cuda.synchronize()
+    assert M[4].float().mean().item() >= 0.9          # S:260 reuse >= 0.9
+    Zc = Z.cpu().double()
+    cos = (Zc[4] @ Zc[0]) / Zc[4].norm() / Zc[0].norm()
+    assert cos.item() >= 0.999
