@@ -94,6 +94,16 @@ typedef struct {
 #define RV_DENSE 2u        /* ignore the gates: every token recomputed (own-dense baseline)     */
 #define RV_FORCE_MASKS 4u  /* masks is an INPUT [n][L][N]: forced reuse map (diagnostic, Q18)   */
 #define RV_NO_GRAPH 8u     /* launch kernels directly instead of through a cached CUDA graph    */
+#define RV_PROFILE 16u     /* time every kernel launch with CUDA events (see rv_profile)         */
+
+/* Per-kernel-class profile of the last RV_PROFILE embed (rv_profile). */
+typedef struct {
+  char name[24];       /* kernel class, e.g. "gemm_fc1", "score", "attention"               */
+  int32_t launches;    /* launches of this class in the embed                               */
+  double ms;           /* summed CUDA-event durations of those launches                     */
+  double flops;        /* algorithmic tensor FLOPs (2*M*N*K with the actual compacted M)    */
+  double bytes;        /* algorithmic HBM bytes (DESIGN.md §6 per-row byte model)            */
+} rv_kernel_prof;
 
 /* Create a context on CUDA device `device`.  Validates cfg (RV_ECONFIG) and requires a
  * compute-capability-10.x device (RV_ECUDA otherwise). */
@@ -144,6 +154,11 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
 
 /* Wait for the in-flight embed; fill *stats if non-NULL.  RV_ECUDA on a kernel fault. */
 rv_status rv_wait(rv_ctx* ctx, rv_stats* stats);
+
+/* After rv_wait of an embed launched with RV_PROFILE: fill up to max_entries per-class
+ * records (classes with at least one launch, pipeline order) and return how many were
+ * written, or a negative rv_status.  Event durations are taken on the embed's stream. */
+int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries);
 
 /* Human-readable message for the last error on ctx (never NULL; "" when none).  With
  * ctx == NULL returns the last rv_create failure message. */

@@ -17,7 +17,7 @@ P_f32 = ctypes.POINTER(ctypes.c_float)
 RV_OK = 0
 STATUS = {0: "RV_OK", -1: "RV_ECONFIG", -2: "RV_ESHAPE", -3: "RV_EPLAN", -4: "RV_ECACHE",
           -5: "RV_ECONTRACT", -6: "RV_ECUDA", -7: "RV_ENOMEM", -8: "RV_EBUSY"}
-RV_DEVICE_PTRS, RV_DENSE, RV_FORCE_MASKS, RV_NO_GRAPH = 1, 2, 4, 8
+RV_DEVICE_PTRS, RV_DENSE, RV_FORCE_MASKS, RV_NO_GRAPH, RV_PROFILE = 1, 2, 4, 8, 16
 RV_I, RV_P, RV_B2, RV_B1 = 0, 1, 2, 3
 
 
@@ -39,6 +39,11 @@ class RvStats(ctypes.Structure):
                 ("reuse_by_layer", ctypes.c_float * 64)]
 
 
+class RvKernelProf(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("launches", c_i32), ("ms", ctypes.c_double),
+                ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
 class ReuseViTError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
@@ -56,6 +61,7 @@ SIGNATURES = {
     "rv_plan_check": (c_i32, [ctypes.POINTER(RvPlan)]),
     "rv_embed": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(RvPlan), c_u32, c_vp, c_vp, c_vp, c_vp]),
     "rv_wait": (c_i32, [c_vp, ctypes.POINTER(RvStats)]),
+    "rv_profile": (c_i32, [c_vp, ctypes.POINTER(RvKernelProf), c_i32]),
     "rv_last_error": (ctypes.c_char_p, [c_vp]),
     "rv_status_string": (ctypes.c_char_p, [c_i32]),
     "rv_destroy": (None, [c_vp]),

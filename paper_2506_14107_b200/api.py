@@ -16,8 +16,8 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_NO_GRAPH, RvConfig, RvPlan, RvStats,
-                   check, load_library)
+from ._lib import (RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_NO_GRAPH, RV_PROFILE, RvConfig,
+                   RvKernelProf, RvPlan, RvStats, check, load_library)
 
 __all__ = ["ReuseViT", "plan_gop", "plan_check", "vit_blob_floats", "gate_blob_floats"]
 
@@ -114,7 +114,8 @@ class ReuseViT:
     # ------------------------------------------------------------------ embed
     def embed_async(self, patches, codec, plan: Optional[dict] = None, *, refresh: int = 20,
                     reorder: bool = True, dense: bool = False, force_masks=None, want_masks: bool = True,
-                    want_scores: bool = False, stream=None, graph: bool = True, out=None):
+                    want_scores: bool = False, stream=None, graph: bool = True, out=None,
+                    profile: bool = False):
         """Enqueue one embed; returns a handle for ``wait``.  ``out`` optionally supplies the
         output buffers (emb, masks, scores) to reuse across calls (same pointers -> the
         cached CUDA graph is replayed)."""
@@ -125,7 +126,7 @@ class ReuseViT:
         st, keep = _plan_struct(plan)
         L, N, D = self.cfg.layers, self.N, self.cfg.dim
         device_path = isinstance(patches, torch.Tensor) and patches.is_cuda
-        flags = (RV_DENSE if dense else 0) | (0 if graph else RV_NO_GRAPH)
+        flags = (RV_DENSE if dense else 0) | (0 if graph else RV_NO_GRAPH) | (RV_PROFILE if profile else 0)
         if force_masks is not None:
             flags |= RV_FORCE_MASKS
         if device_path:
@@ -172,6 +173,15 @@ class ReuseViT:
                 "peak_cache_bytes": int(s.peak_cache_bytes), "keepall_cache_bytes": int(s.keepall_cache_bytes),
                 "ms_total": s.ms_total, "ms_compute": s.ms_compute, "n_levels": s.n_levels,
                 "n_launches": s.n_launches, "reuse_by_layer": list(s.reuse_by_layer[:L])}
+
+    def profile(self) -> list:
+        """Per-kernel-class records of the last ``profile=True`` embed (after ``wait``)."""
+        buf = (RvKernelProf * 32)()
+        k = self.lib.rv_profile(self.h, buf, 32)
+        if k < 0:
+            check(self.lib, k, self.h)
+        return [{"name": buf[i].name.decode(), "launches": buf[i].launches, "ms": buf[i].ms,
+                 "flops": buf[i].flops, "bytes": buf[i].bytes} for i in range(k)]
 
     def embed(self, patches, codec, plan: Optional[dict] = None, **kw):
         """Synchronous embed: returns (Z [n,D], masks [n,L,N] or None, scores or None, stats)."""

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
     compact_kernel(int n_w, int T, const int4* __restrict__ wdesc, const uint8_t* __restrict__ wmask,
                    const uint8_t* __restrict__ wprov, const int* __restrict__ cntC, int* __restrict__ idxC,
                    int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
-                   int* __restrict__ counts, unsigned long long* reuse_ctr) {
+                   int* __restrict__ counts, unsigned long long* reuse_ctr, int* count_log) {
   __shared__ int s_part[COMPACT_THREADS / 32];
   __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
   __shared__ int s_base[2];
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
       counts[0] = tot;
       counts[1] = n_w * T - tot;
       if (reuse_ctr) atomicAdd(reuse_ctr, (unsigned long long)(n_w * T - tot));
+      if (count_log) { count_log[0] = tot; count_log[1] = n_w * T - tot; }
     }
   }
   __syncthreads();
@@ -188,10 +189,10 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
 
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
-                           unsigned long long* reuse_ctr, cudaStream_t s) {
+                           unsigned long long* reuse_ctr, int* count_log, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
   compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
-                                                 cntC, idxC, idxR, provrow, qoff, counts, reuse_ctr);
+                                                 cntC, idxC, idxR, provrow, qoff, counts, reuse_ctr, count_log);
   return cudaGetLastError();
 }
 

@@ -93,7 +93,23 @@ struct rv_ctx {
   cudaStream_t cur_stream = nullptr;
   std::vector<Wave> waves;
   std::vector<int> wdesc_host;
+  // ---- profiling (RV_PROFILE): event pairs around every launch + per-wave counts log
+  struct ProfRec { int cls, l, w; cudaEvent_t a, b; };
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  std::vector<ProfRec> prof_recs;
+  int* count_log = nullptr;          // [L][n_waves][2] = {M_C, M_R}
+  int count_log_cap = 0;
+  bool prof_valid = false;
+  std::vector<rv_kernel_prof> prof_out;
 };
+
+enum { K_PATCH, K_PE, K_EMBED, K_SCORE, K_COMPACT, K_GATHER, K_QKV, K_RGATHER, K_ATTN, K_CLS, K_WO, K_LN2,
+       K_FC1, K_FC2, K_R1, K_R2, K_LNPOST, K_NCLS };
+static const char* kClsName[K_NCLS] = {"patch_to_bf16", "gemm_pe", "embed_finish", "score", "compact",
+                                       "gather_ln1", "gemm_qkv", "rgather", "attention", "cls_prob",
+                                       "gemm_wo", "ln2", "gemm_fc1", "gemm_fc2", "gemm_r1", "gemm_r2",
+                                       "ln_post"};
 
 namespace {
 
@@ -185,6 +201,15 @@ rv_status upload_f(rv_ctx* ctx, std::vector<void*>& list, float** dst, const flo
 void free_list(std::vector<void*>& l) {
   for (void* p : l) cudaFree(p);
   l.clear();
+}
+
+cudaEvent_t ctx_event(rv_ctx* ctx) {
+  if (ctx->prof_used == ctx->prof_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->prof_pool.push_back(e);
+  }
+  return ctx->prof_pool[ctx->prof_used++];
 }
 
 // ------------------------------------------------------------------ plan helpers
@@ -294,9 +319,27 @@ struct Rec {
   int launches = 0;
   cudaError_t err = cudaSuccess;
   const char* where = "";
+  bool prof = false;
+  int cur_cls = -1, cur_l = -1, cur_w = -1;
+  cudaEvent_t cur_ev = nullptr;
+  // Start a timed launch of kernel class `cls` (profiling embeds only).
+  void begin(int cls, int l, int wi) {
+    if (!prof || err != cudaSuccess) return;
+    cur_cls = cls; cur_l = l; cur_w = wi;
+    cur_ev = ctx_event(ctx);
+    cudaError_t e = cudaEventRecordWithFlags(cur_ev, s, cudaEventRecordExternal);
+    if (e != cudaSuccess && err == cudaSuccess) { err = e; where = "event"; }
+  }
   void chk(cudaError_t e, const char* w) {
     ++launches;
     if (e != cudaSuccess && err == cudaSuccess) { err = e; where = w; }
+    if (prof && cur_cls >= 0 && err == cudaSuccess) {
+      cudaEvent_t end = ctx_event(ctx);
+      cudaError_t e2 = cudaEventRecordWithFlags(end, s, cudaEventRecordExternal);
+      if (e2 != cudaSuccess && err == cudaSuccess) { err = e2; where = "event"; }
+      ctx->prof_recs.push_back({cur_cls, cur_l, cur_w, cur_ev, end});
+    }
+    cur_cls = -1;
   }
 };
 
@@ -309,6 +352,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
   --r.launches;
   // a1: patch embed (dense, all frames): bf16 operand, GEMM into X0 rows f*T+1+i, finish.
+  r.begin(K_PATCH,-1,-1);
   r.chk(launch_patch_to_bf16(patches, ctx->patches_bf16, (long long)n * N, ctx->pp, ctx->KP, s), "patch_to_bf16");
   {
     Epi e;
@@ -316,30 +360,37 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
     e.out_ld = D;
     e.row_div = N;
     e.row_add = 1;
+    r.begin(K_PE,-1,-1);
     r.chk(gemm_launch(ctx->pe, nullptr, n * N, n * N, e, s), "gemm_pe");
   }
+  r.begin(K_EMBED,-1,-1);
   r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pcls, n, T, D, N, s),
         "embed_finish");
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
     float* Xin = ctx->X[l & 1];
     float* Xout = ctx->X[(l + 1) & 1];
-    for (const Wave& wv : ctx->waves) {
+    for (int wi = 0; wi < (int)ctx->waves.size(); ++wi) {
+      const Wave& wv = ctx->waves[wi];
       const int n_w = wv.n_w;
       const int* wd = ctx->wdesc + (size_t)wv.off * 4;
       const int maxC = n_w * T, maxR = n_w * N;
       // a2-a3: Eq. 1-4
+      r.begin(K_SCORE,l,wi);
       r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pcls, codec, force ? masks : nullptr,
                          ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
                          ctx->wprov, ctx->cntC, s),
             "score");
       // a4: Eq. 5-6 stream compaction
+      r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntC, ctx->idxC, ctx->idxR, ctx->provrow,
-                           ctx->qoff, ctx->counts, ctx->reuse_ctr + l, s),
+                           ctx->qoff, ctx->counts, ctx->reuse_ctr + l,
+                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, s),
             "compact");
       const int* MC = ctx->counts;
       const int* MR = ctx->counts + 1;
       // a5: gather + LN1
+      r.begin(K_GATHER,l,wi);
       r.chk(launch_gather_ln(Xin, ctx->idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, ctx->A, D, s), "gather_ln1");
       // a6: QKV; q compact, K/V scattered to the cache rows of C
       {
@@ -353,13 +404,15 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out2_rows = ctx->idxC;
         e.out2_ld = 2LL * D;
         e.out2_bf16 = 1;
+        r.begin(K_QKV,l,wi);
         r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
       }
       // a7 + Eq. 8: reused rows take the provider's K/V; Delta for the restoration layer
-      if (wv.any_ref) r.chk(launch_rgather(Xin, ctx->KV, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather");
+      if (wv.any_ref) { r.begin(K_RGATHER,l,wi); r.chk(launch_rgather(Xin, ctx->KV, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather"); }
       // a8: attention over all T keys; CLS row -> t for layer l+1
+      r.begin(K_ATTN,l,wi);
       r.chk(launch_attention(ctx->q, ctx->KV, ctx->att, wd, ctx->qoff, n_w, T, D, H, s), "attention");
-      if (!dense && l + 1 < L) r.chk(launch_cls_prob(ctx->q, ctx->KV, wd, ctx->qoff, ctx->pcls, n_w, T, D, H, s), "cls_prob");
+      if (!dense && l + 1 < L) { r.begin(K_CLS,l,wi); r.chk(launch_cls_prob(ctx->q, ctx->KV, wd, ctx->qoff, ctx->pcls, n_w, T, D, H, s), "cls_prob"); }
       // a9: W_o + residual (gathered X_{l-1} rows)
       {
         Epi e;
@@ -369,9 +422,11 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.resid_ld = D;
         e.out = ctx->x1;
         e.out_ld = D;
+        r.begin(K_WO,l,wi);
         r.chk(gemm_launch(ctx->g_wo[l], MC, 0, maxC, e, s), "gemm_wo");
       }
       // a10: LN2 + FC1 + QuickGELU
+      r.begin(K_LN2,l,wi);
       r.chk(launch_gather_ln(ctx->x1, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
       {
         Epi e;
@@ -380,6 +435,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out = ctx->h;
         e.out_ld = F;
         e.out_bf16 = 1;
+        r.begin(K_FC1,l,wi);
         r.chk(gemm_launch(ctx->g_fc1[l], MC, 0, maxC, e, s), "gemm_fc1");
       }
       // a11: FC2 + residual, scattered to X_l rows of C (Eq. 10, C side)
@@ -391,6 +447,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out = Xout;
         e.out_rows = ctx->idxC;
         e.out_ld = D;
+        r.begin(K_FC2,l,wi);
         r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
       }
       // a12: restoration (Eq. 9) + merge (Eq. 10, R side)
@@ -401,6 +458,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e1.out = ctx->hr;
         e1.out_ld = Hr;
         e1.out_bf16 = 1;
+        r.begin(K_R1,l,wi);
         r.chk(gemm_launch(ctx->g_r1[l], MR, 0, maxR, e1, s), "gemm_r1");
         Epi e2;
         e2.bias = w.br2;
@@ -410,11 +468,13 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e2.out = Xout;
         e2.out_rows = ctx->idxR;
         e2.out_ld = D;
+        r.begin(K_R2,l,wi);
         r.chk(gemm_launch(ctx->g_r2[l], MR, 0, maxR, e2, s), "gemm_r2");
       }
     }
   }
   // a14: Z = LN_post(CLS), slots are display indices
+  r.begin(K_LNPOST,-1,-1);
   r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
 }
 
@@ -658,6 +718,17 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   if (total_desc != n) return fail(ctx, RV_EPLAN, "rv_embed: internal wave bookkeeping mismatch");
   if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w)))
     return st;
+  {
+    const int need = L * (int)ctx->waves.size() * 2;
+    if (need > ctx->count_log_cap) {
+      if (ctx->count_log) cudaFree(ctx->count_log);
+      ctx->count_log = nullptr;
+      CK(cudaMalloc(&ctx->count_log, need * sizeof(int)));
+      ctx->count_log_cap = need;
+      if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    }
+  }
+  ctx->prof_valid = false;
   cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : nullptr;
   const bool devp = flags & RV_DEVICE_PTRS;
   const float* d_patches = devp ? patches : ctx->in_patches;
@@ -689,13 +760,18 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
                                 (long long)(intptr_t)ws, ctx->capC, ctx->capR};
   for (int v : ctx->wdesc_host) key.push_back(v);
   Rec rec{ctx, ws};
+  rec.prof = (flags & RV_PROFILE) != 0;
   if (flags & RV_NO_GRAPH) {
+    ctx->prof_used = 0;
+    ctx->prof_recs.clear();
     record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
     if (rec.err != cudaSuccess) return fail(ctx, RV_ECUDA, "launch %s: %s", rec.where, cudaGetErrorString(rec.err));
   } else {
     if (!ctx->gexec || key != ctx->gkey) {
       if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
       cudaGraph_t g = nullptr;
+      ctx->prof_used = 0;
+      ctx->prof_recs.clear();
       CK(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
       record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
       cudaError_t ce = cudaStreamEndCapture(ws, &g);
@@ -729,6 +805,7 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   ctx->cur_levels = (int)levels.size();
   ctx->cur_launches = rec.launches;
   ctx->cur_stream = ws;
+  ctx->prof_valid = rec.prof;
   return RV_OK;
 }
 
@@ -782,9 +859,73 @@ void rv_destroy(rv_ctx* ctx) {
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   free_list(ctx->ballocs);
   free_list(ctx->wallocs);
+  if (ctx->count_log) cudaFree(ctx->count_log);
+  for (auto e : ctx->prof_pool) cudaEventDestroy(e);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
+}
+
+int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
+  if (!ctx || !out) return RV_ECONTRACT;
+  if (!ctx->prof_valid || ctx->inflight)
+    return fail(ctx, RV_ECONTRACT, "rv_profile: no completed RV_PROFILE embed (call rv_wait first)");
+  CK(cudaSetDevice(ctx->device));
+  const int nwv = (int)ctx->waves.size();
+  std::vector<int> log((size_t)ctx->L * nwv * 2);
+  CK(cudaMemcpy(log.data(), ctx->count_log, log.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  const double D = ctx->D, T = ctx->T, N = ctx->N, F = ctx->F, Hr = ctx->Hr, n = ctx->cur_n;
+  // per-wave host facts: frames, decision frames and their reference rows
+  std::vector<double> wdec(nwv, 0), wrefs(nwv, 0);
+  for (int wi = 0; wi < nwv; ++wi) {
+    const Wave& wv = ctx->waves[wi];
+    for (int j = 0; j < wv.n_w; ++j) {
+      const int* d = &ctx->wdesc_host[(size_t)(wv.off + j) * 4];
+      if (d[3] != RV_I) { wdec[wi] += 1; wrefs[wi] += (d[1] >= 0) + (d[2] >= 0); }
+    }
+  }
+  std::vector<rv_kernel_prof> acc(K_NCLS);
+  for (int c = 0; c < K_NCLS; ++c) {
+    memset(&acc[c], 0, sizeof(rv_kernel_prof));
+    snprintf(acc[c].name, sizeof acc[c].name, "%s", kClsName[c]);
+  }
+  for (const auto& r : ctx->prof_recs) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    rv_kernel_prof& a = acc[r.cls];
+    a.launches += 1;
+    a.ms += ms;
+    double MC = 0, MR = 0, nw = 0;
+    if (r.l >= 0) {
+      MC = log[((size_t)r.l * nwv + r.w) * 2];
+      MR = log[((size_t)r.l * nwv + r.w) * 2 + 1];
+      nw = ctx->waves[r.w].n_w;
+    }
+    // Algorithmic FLOPs (tensor work) and HBM bytes of this launch.
+    switch (r.cls) {
+      case K_PATCH: a.bytes += n * N * (ctx->pp * 4.0 + ctx->KP * 2.0); break;
+      case K_PE: a.flops += 2.0 * n * N * ctx->pp * D; a.bytes += n * N * (ctx->KP * 2.0 + D * 4.0); break;
+      case K_EMBED: a.bytes += n * T * D * 8.0; break;
+      case K_SCORE: a.bytes += (wdec[r.w] + wrefs[r.w]) * N * D * 4.0 + wdec[r.w] * N * 10.0; break;
+      case K_COMPACT: a.bytes += nw * T * 2.0 + (MC + 2 * MR) * 4.0; break;
+      case K_GATHER: a.bytes += MC * (D * 4.0 + D * 2.0 + 4.0); break;
+      case K_QKV: a.flops += 2.0 * MC * 3 * D * D; a.bytes += MC * (D * 2.0 + 3 * D * 2.0) + 3 * D * D * 2.0; break;
+      case K_RGATHER: a.bytes += MR * (2 * D * 4.0 + D * 2.0 + 2 * (2 * D * 2.0) + 8.0); break;
+      case K_ATTN: a.flops += 4.0 * MC * T * D; a.bytes += MC * D * 4.0 + nw * T * 2 * D * 2.0; break;
+      case K_CLS: a.bytes += nw * (T * D * 2.0 + D * 2.0 + N * 4.0); break;
+      case K_WO: a.flops += 2.0 * MC * D * D; a.bytes += MC * (D * 2.0 + D * 4.0 + D * 4.0) + D * D * 2.0; break;
+      case K_LN2: a.bytes += MC * (D * 4.0 + D * 2.0); break;
+      case K_FC1: a.flops += 2.0 * MC * F * D; a.bytes += MC * (D * 2.0 + F * 2.0) + F * D * 2.0; break;
+      case K_FC2: a.flops += 2.0 * MC * D * F; a.bytes += MC * (F * 2.0 + D * 4.0 + D * 4.0) + F * D * 2.0; break;
+      case K_R1: a.flops += 2.0 * MR * Hr * D; a.bytes += MR * (D * 2.0 + Hr * 2.0) + Hr * D * 2.0; break;
+      case K_R2: a.flops += 2.0 * MR * D * Hr; a.bytes += MR * (Hr * 2.0 + D * 4.0 * 2) + Hr * D * 2.0; break;
+      case K_LNPOST: a.bytes += n * D * 8.0; break;
+    }
+  }
+  int k = 0;
+  for (int c = 0; c < K_NCLS && k < max_entries; ++c)
+    if (acc[c].launches) out[k++] = acc[c];
+  return k;
 }
 
 // ---------------------------------------------------------------------- stage entry points
@@ -805,7 +946,7 @@ rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const
                            int32_t* provrow, int32_t* qoff, int32_t* counts, void* stream) {
   if (!ctx) return RV_ECONTRACT;
   CK(cudaSetDevice(ctx->device));
-  CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntC, idxC, idxR, provrow, qoff, counts, nullptr,
+  CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntC, idxC, idxR, provrow, qoff, counts, nullptr, nullptr,
                     (cudaStream_t)stream));
   return RV_OK;
 }

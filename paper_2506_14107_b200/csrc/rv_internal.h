@@ -64,7 +64,7 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
                          int* cntC, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
-                           unsigned long long* reuse_ctr, cudaStream_t s);
+                           unsigned long long* reuse_ctr, int* count_log, cudaStream_t s);
 
 // ---------------------------------------------------------------- attention (k_attn.cu)
 cudaError_t launch_attention(const bf16* q, const bf16* KV, bf16* out, const int* wdesc, const int* qoff, int n_w,
