@@ -53,7 +53,7 @@ typedef struct rv_ctx rv_ctx;
 /* Model dimensions (SPEC.md:97-100 ViTConfig; SURVEY §8 notation).
  *   N = (img/patch)^2 patch tokens, T = N + 1 with CLS, pp = 3*patch^2 pixels per patch.
  *   Requirements: dim % heads == 0, dim/heads in {16, 64}, dim % 64 == 0, ffn % 64 == 0,
- *   hidden_r % 64 == 0, 1 <= hidden_g <= 32, img % patch == 0, layers <= 64, T <= 1024. */
+ *   hidden_r % 64 == 0, 1 <= hidden_g <= 32, img % patch == 0, layers <= 64, T <= 768. */
 typedef struct {
   int32_t layers, dim, heads, patch, img, ffn, hidden_r, hidden_g;
 } rv_config;

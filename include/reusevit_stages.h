@@ -26,19 +26,19 @@ extern "C" {
  * force != NULL).  t [slots][N] and codec [slots][N] fp32.  Writes
  *   masks [slots][L][N] u8 and scores [slots][L][N] fp32 (NaN for I frames) at `layer`,
  *   wmask [n_w][T] u8 (wave-local M, token 0 = 0), wprov [n_w][T] u8 (0 past, 1 future),
- *   cntC [n_w] int32 = |C| of each frame (CLS included).                                  */
+ *   cntR [n_w] int32 = |R| of each frame (reused patch tokens).                             */
 rv_status rv_stage_score(rv_ctx* ctx, int32_t layer, const float* X, int32_t n_w,
                          const int32_t* wdesc, const float* t, const float* codec,
                          const uint8_t* force, uint8_t* masks, float* scores,
-                         uint8_t* wmask, uint8_t* wprov, int32_t* cntC, void* stream);
+                         uint8_t* wmask, uint8_t* wprov, int32_t* cntR, void* stream);
 
 /* a4 — Eq. 5-6 filtration as stream compaction (§5.3): from wmask,
- * wprov and cntC, writes idxC [<= n_w*T] (global rows of C, frames in wave order, tokens
+ * wprov and cntR, writes idxC [<= n_w*T] (global rows of C, frames in wave order, tokens
  * ascending, CLS first), idxR / provrow [<= n_w*N] (global rows of R and of their
  * providers' same token), qoff [n_w+1] (exclusive prefix of |C|), counts[2] = {M_C, M_R}.
  * Bit-exact given the mask; all counts stay on the device. */
 rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
-                           const uint8_t* wmask, const uint8_t* wprov, const int32_t* cntC,
+                           const uint8_t* wmask, const uint8_t* wprov, const int32_t* cntR,
                            int32_t* idxC, int32_t* idxR, int32_t* provrow, int32_t* qoff,
                            int32_t* counts, void* stream);
 
@@ -46,7 +46,7 @@ rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
  * out[m][n] = act(sum_k A[m][k] * B[n][k] + bias[n]) for m < M, n < N, with A bf16
  * [M][K] row-major, B bf16 [N][K] row-major (i.e. out = A * B^T), bias fp32 [N] or NULL,
  * act 0 = identity, 1 = QuickGELU; out fp32 (out_bf16 == 0) or bf16 [M][N].
- * K % 64 == 0, N % 16 == 0. */
+ * K % 64 == 0, N % 64 == 0 (RV_ECONTRACT otherwise). */
 rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void* A,
                         const void* B, const float* bias, int32_t act, void* out,
                         int32_t out_bf16, void* stream);
@@ -54,8 +54,9 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
 /* a8 — attention of compacted queries over all T keys of their frame:
  * q [M_C][D] bf16 (rows qoff[w]..qoff[w+1]-1 belong to wave frame w, first row = CLS),
  * KV [slots][T][2D] bf16 (K in columns 0..D-1, V in D..2D-1, head h = columns h*dh..),
- * out [M_C][D] bf16 = softmax(q K^T / sqrt(dh)) V per head; pcls [slots][N] fp32 = head
- * mean of the CLS softmax row over patch keys (t for the next layer). */
+ * out [M_C][D] bf16 = softmax(q K^T / sqrt(dh)) V per head; pcls [slots][H][N] fp32 (or
+ * NULL) = per-head CLS softmax row over the patch keys; its head mean is t for the next
+ * layer. */
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
                              const int32_t* qoff, const void* q, const void* KV, void* out,
                              float* pcls, void* stream);

@@ -190,14 +190,14 @@ class ReuseViT:
         return hnd["emb"], hnd["masks"], hnd["scores"], stats
 
     # ------------------------------------------------------------------ stages (tests)
-    def stage_score(self, layer, X, wdesc, t, codec, force, masks, scores, wmask, wprov, cntC, stream):
+    def stage_score(self, layer, X, wdesc, t, codec, force, masks, scores, wmask, wprov, cntR, stream):
         check(self.lib, self.lib.rv_stage_score(self.h, layer, _ptr(X), wdesc.shape[0], _ptr(wdesc), _ptr(t),
                                                 _ptr(codec), _ptr(force), _ptr(masks), _ptr(scores), _ptr(wmask),
-                                                _ptr(wprov), _ptr(cntC), ctypes.c_void_p(stream.cuda_stream)), self.h)
+                                                _ptr(wprov), _ptr(cntR), ctypes.c_void_p(stream.cuda_stream)), self.h)
 
-    def stage_compact(self, wdesc, wmask, wprov, cntC, idxC, idxR, provrow, qoff, counts, stream):
+    def stage_compact(self, wdesc, wmask, wprov, cntR, idxC, idxR, provrow, qoff, counts, stream):
         check(self.lib, self.lib.rv_stage_compact(self.h, wdesc.shape[0], _ptr(wdesc), _ptr(wmask), _ptr(wprov),
-                                                  _ptr(cntC), _ptr(idxC), _ptr(idxR), _ptr(provrow), _ptr(qoff),
+                                                  _ptr(cntR), _ptr(idxC), _ptr(idxR), _ptr(provrow), _ptr(qoff),
                                                   _ptr(counts), ctypes.c_void_p(stream.cuda_stream)), self.h)
 
     def stage_gemm(self, A, B, bias=None, act=0, out=None, out_bf16=False, stream=None):

@@ -1,23 +1,26 @@
 // k_attn.cu — attention of the compacted queries over all T keys of their frame
 // (SURVEY §8(a) a8).  Every recomputed query attends to all tokens of its frame (P:313:
-// attention "involves interactions among all tokens"); reused tokens contribute the K/V
-// copied from their provider (a7).  One CTA = (64 compacted query rows of one frame, one
-// head): K, V of that frame/head staged in shared memory, S = Q K^T and O = P V on the
-// tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate), online softmax in fp32 with
-// exp2 and max subtraction.  Queries are variable per frame (qoff from the compaction
-// kernel, read on the device); CTAs past a frame's query count exit at once.
+// attention "involves interactions among all tokens").  Reused tokens contribute the K/V of
+// their provider through the kvsrc row table written by the compaction kernel (a7: the reuse
+// cache is read in place, chains resolved at write time, no copy).
 //
-// cls_prob_kernel: t for the next layer = head-mean of the CLS softmax row over the patch
-// keys ("attention weights from the class token"), fp32, fixed summation
-// order over heads (deterministic).
+// One CTA = (one frame of the wave, one head), 4 warps x 16 query rows per q-tile, looping
+// over all q-tiles of the frame with K/V resident in shared memory:
+//   * K/V rows gathered with cp.async (16 B, L2-only) in 64-key commit groups, so the first
+//     key blocks are computed while later ones are still in flight;
+//   * S = Q K^T and O = P V on the tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate;
+//     V fragments via ldmatrix.trans), online softmax in fp32 with exp2 and max subtraction;
+//   * the CLS query (first compact row of every frame) additionally emits its normalised
+//     softmax row over the patch keys for this head: pclsh[slot][h][j-1];
+//     the score kernel of the next layer averages the H heads in a fixed order.
 #include "common.cuh"
 #include "rv_internal.h"
 
 namespace rv {
 namespace {
 
-constexpr int QT = 64;   // query rows per CTA (4 warps x 16)
-constexpr int KB = 64;   // keys per online-softmax block
+constexpr int QT = 64;   // query rows per q-tile (4 warps x 16)
+constexpr int KB = 64;   // keys per online-softmax block / cp.async commit group
 
 RV_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -26,233 +29,232 @@ RV_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+RV_DEV void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+RV_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+RV_DEV void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+template <int DH>
+RV_DEV void load_kv_block(bf16* Kb, bf16* Vb, const bf16* __restrict__ KV, const int* rows_s, int k0, int Tp, int T,
+                          long long ld, int D, int h, int tid) {
+  constexpr int KS = DH + 8, CH = DH / 8;
+  const int nrow = min(KB, Tp - k0);
+  for (int idx = tid; idx < nrow * CH; idx += 128) {
+    const int j = idx / CH, c = idx % CH;
+    const bool ok = k0 + j < T;
+    const bf16* kr = KV + (long long)rows_s[k0 + j] * ld + h * DH + c * 8;
+    cp_async16(Kb + j * KS + c * 8, kr, ok);
+    cp_async16(Vb + j * KS + c * 8, kr + D, ok);
+  }
+}
 
+// One CTA = (frame w of the wave, head h).  Q tile (64 rows) resident; K/V streamed in 64-key
+// blocks through a 2-deep cp.async ring (the next block lands while this one is computed), so
+// ~45 KB of shared memory per CTA and several CTAs per SM keep the memory system busy.
 template <int DH>
 __global__ void __launch_bounds__(128)
-    attn_kernel(const bf16* __restrict__ q, const bf16* __restrict__ KV, bf16* __restrict__ out,
-                const int4* __restrict__ wdesc, const int* __restrict__ qoff, int T, int D,
-                float scale_log2) {
-  constexpr int KS = DH + 8;  // padded row stride (bf16) of Ks / Qs: conflict-free fragments
-  const int w = blockIdx.z, h = blockIdx.y, qt = blockIdx.x;
+    attn_kernel(const bf16* __restrict__ q, const bf16* __restrict__ KV, const int* __restrict__ kvsrc,
+                bf16* __restrict__ out, const int4* __restrict__ wdesc, const int* __restrict__ qoff,
+                float* __restrict__ pclsh, int T, int D, int H, float scale_log2) {
+  constexpr int KS = DH + 8;     // padded row stride (bf16): conflict-free fragments / ldmatrix
+  constexpr int CH = DH / 8;     // 16-byte chunks per row
+  const int h = blockIdx.x, w = blockIdx.y;
   const int q0 = qoff[w];
   const int nq = qoff[w + 1] - q0;
-  if (qt * QT >= nq) return;
   const int slot = wdesc[w].x;
-  const int Tp = (T + KB - 1) / KB * KB;
+  const int Tp = (T + 15) / 16 * 16;        // keys padded to the mma k-step
+  const int nkb = (Tp + KB - 1) / KB;
   extern __shared__ __align__(16) unsigned char attn_smem[];
-  bf16* Ks = reinterpret_cast<bf16*>(attn_smem);  // [Tp][KS]
-  bf16* Vs = Ks + Tp * KS;                        // [Tp][KS]
-  bf16* Qs = Vs + Tp * KS;                        // [QT][KS]
+  bf16* Kr = reinterpret_cast<bf16*>(attn_smem);    // ring [2][KB][KS]
+  bf16* Vr = Kr + 2 * KB * KS;                       // ring [2][KB][KS]
+  bf16* Qs = Vr + 2 * KB * KS;                       // [QT][KS]
+  int* rows_s = reinterpret_cast<int*>(Qs + QT * KS);  // [Tp] K/V source row of every key
+  float* scls = reinterpret_cast<float*>(rows_s + Tp); // [Tp] raw CLS logits (q_cls . k_j)
+  __shared__ float s_cls[2];                          // CLS row max / sum
   const long long ld = 2LL * D;
-  const bf16* Kg = KV + (long long)slot * T * ld + h * DH;
-  const bf16* Vg = Kg + D;
-  constexpr int CH = DH / 8;  // 16-byte chunks per row
-  const uint4 zero = make_uint4(0, 0, 0, 0);
-  for (int idx = threadIdx.x; idx < Tp * CH; idx += blockDim.x) {
-    const int j = idx / CH, c = idx % CH;
-    const uint4 kv = j < T ? *reinterpret_cast<const uint4*>(Kg + j * ld + c * 8) : zero;
-    *reinterpret_cast<uint4*>(Ks + j * KS + c * 8) = kv;
-    const uint4 vv = j < T ? *reinterpret_cast<const uint4*>(Vg + j * ld + c * 8) : zero;
-    *reinterpret_cast<uint4*>(Vs + j * KS + c * 8) = vv;
-  }
-  for (int idx = threadIdx.x; idx < QT * CH; idx += blockDim.x) {
-    const int r = idx / CH, c = idx % CH;
-    const int row = qt * QT + r;
-    const uint4 qv = row < nq ? *reinterpret_cast<const uint4*>(q + (long long)(q0 + row) * D + h * DH + c * 8) : zero;
-    *reinterpret_cast<uint4*>(Qs + r * KS + c * 8) = qv;
-  }
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int r0 = warp * 16;
-  uint32_t qa[DH / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < DH / 16; ++kk) {
-    qa[kk][0] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g) * KS + kk * 16 + 2 * tq);
-    qa[kk][1] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g + 8) * KS + kk * 16 + 2 * tq);
-    qa[kk][2] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g) * KS + kk * 16 + 8 + 2 * tq);
-    qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g + 8) * KS + kk * 16 + 8 + 2 * tq);
-  }
-  float o[DH / 8][4];
-#pragma unroll
-  for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-  for (int kb = 0; kb < Tp; kb += KB) {
-    float s[KB / 8][4];
-#pragma unroll
-    for (int j = 0; j < KB / 8; ++j) {
-      s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk) {
-        const bf16* kr = Ks + (kb + j * 8 + g) * KS + kk * 16 + 2 * tq;
-        mma16816(s[j], qa[kk], *reinterpret_cast<const uint32_t*>(kr), *reinterpret_cast<const uint32_t*>(kr + 8));
-      }
-      const int col = kb + j * 8 + 2 * tq;
-      if (col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
-      if (col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
-    }
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < KB / 8; ++j) {
-      mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
-      mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float a0 = exp2f((m0 - mn0) * scale_log2), a1 = exp2f((m1 - mn1) * scale_log2);
-    const float ms0 = mn0 * scale_log2, ms1 = mn1 * scale_log2;
-    float rs0 = 0.f, rs1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < KB / 8; ++j) {
-      s[j][0] = exp2f(fmaf(s[j][0], scale_log2, -ms0));
-      s[j][1] = exp2f(fmaf(s[j][1], scale_log2, -ms0));
-      s[j][2] = exp2f(fmaf(s[j][2], scale_log2, -ms1));
-      s[j][3] = exp2f(fmaf(s[j][3], scale_log2, -ms1));
-      rs0 += s[j][0] + s[j][1];
-      rs1 += s[j][2] + s[j][3];
-    }
-    l0 = l0 * a0 + rs0;
-    l1 = l1 * a1 + rs1;
-    m0 = mn0;
-    m1 = mn1;
-#pragma unroll
-    for (int i = 0; i < DH / 8; ++i) {
-      o[i][0] *= a0; o[i][1] *= a0; o[i][2] *= a1; o[i][3] *= a1;
-    }
-#pragma unroll
-    for (int kk = 0; kk < KB / 16; ++kk) {
-      uint32_t pa[4];
-      pa[0] = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
-      pa[1] = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
-      pa[2] = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-      pa[3] = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-#pragma unroll
-      for (int dt = 0; dt < DH / 8; dt += 2) {
-        // B fragments of V (row-major [key][dh]) via ldmatrix.trans: lanes 0-15 address keys
-        // kb+16kk+0..15 at column block dt, lanes 16-31 the same keys at column block dt+1.
-        const bf16* vr = Vs + (kb + kk * 16 + (lane & 15)) * KS + (dt + (lane >> 4)) * 8;
-        uint32_t b0, b1, b2, b3;
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                     : "r"((uint32_t)__cvta_generic_to_shared(vr)));
-        mma16816(o[dt], pa, b0, b1);
-        mma16816(o[dt + 1], pa, b2, b3);
-      }
-    }
-  }
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float il0 = 1.f / l0, il1 = 1.f / l1;
-  const int ra = qt * QT + r0 + g, rb = ra + 8;
-#pragma unroll
-  for (int dt = 0; dt < DH / 8; ++dt) {
-    const int col = h * DH + dt * 8 + 2 * tq;
-    if (ra < nq)
-      *reinterpret_cast<uint32_t*>(out + (long long)(q0 + ra) * D + col) = pack_bf16x2(o[dt][0] * il0, o[dt][1] * il0);
-    if (rb < nq)
-      *reinterpret_cast<uint32_t*>(out + (long long)(q0 + rb) * D + col) = pack_bf16x2(o[dt][2] * il1, o[dt][3] * il1);
-  }
-}
+  for (int j = tid; j < Tp; j += 128)
+    rows_s[j] = j < T ? (kvsrc ? __ldg(kvsrc + (long long)slot * T + j) : slot * T + j) : 0;
+  __syncthreads();
 
-__global__ void cls_prob_kernel(const bf16* __restrict__ q, const bf16* __restrict__ KV,
-                                const int4* __restrict__ wdesc, const int* __restrict__ qoff,
-                                float* __restrict__ pcls, int T, int D, int H, int DH, float scale) {
-  extern __shared__ float cls_smem[];
-  float* qs = cls_smem;            // [H][DH]
-  float* ps = qs + H * DH;         // [H][T]
-  const int w = blockIdx.x;
-  const int slot = wdesc[w].x;
-  const long long ld = 2LL * D;
-  const bf16* qrow = q + (long long)qoff[w] * D;   // first compact row of the frame = CLS
-  for (int k = threadIdx.x; k < D; k += blockDim.x) qs[k] = __bfloat162float(qrow[k]);
-  __syncthreads();
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (h < H) {
-    const float* qh = qs + h * DH;
-    const bf16* Kb = KV + (long long)slot * T * ld + h * DH;
-    float mx = -INFINITY;
-    for (int j = lane; j < T; j += 32) {
-      const bf16* kr = Kb + j * ld;
-      float acc = 0.f;
-      for (int k = 0; k < DH; k += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(kr + k);
-        const float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
-        acc += qh[k] * a.x + qh[k + 1] * a.y + qh[k + 2] * b.x + qh[k + 3] * b.y + qh[k + 4] * c.x +
-               qh[k + 5] * c.y + qh[k + 6] * d.x + qh[k + 7] * d.y;
+  const int ntiles = (nq + QT - 1) / QT;
+  for (int qt = 0; qt < ntiles; ++qt) {
+    // Q tile + first key block
+    for (int idx = tid; idx < QT * CH; idx += 128) {
+      const int r = idx / CH, c = idx % CH;
+      const int row = qt * QT + r;
+      const bool ok = row < nq;
+      cp_async16(Qs + r * KS + c * 8, q + (long long)(q0 + (ok ? row : 0)) * D + h * DH + c * 8, ok);
+    }
+    load_kv_block<DH>(Kr, Vr, KV, rows_s, 0, Tp, T, ld, D, h, tid);
+    cp_commit();
+    const bool active = qt * QT + r0 < nq;   // warp-uniform
+    uint32_t qa[DH / 16][4];
+    float o[DH / 8][4];
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int buf = kb & 1;
+      if (kb + 1 < nkb) {       // prefetch the next block into the other ring slot
+        load_kv_block<DH>(Kr + (buf ^ 1) * KB * KS, Vr + (buf ^ 1) * KB * KS, KV, rows_s, (kb + 1) * KB, Tp, T, ld,
+                          D, h, tid);
+        cp_commit();
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
       }
-      acc *= scale;
-      ps[h * T + j] = acc;
-      mx = fmaxf(mx, acc);
+      __syncthreads();
+      if (kb == 0 && active) {
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          qa[kk][0] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g) * KS + kk * 16 + 2 * tq);
+          qa[kk][1] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g + 8) * KS + kk * 16 + 2 * tq);
+          qa[kk][2] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g) * KS + kk * 16 + 8 + 2 * tq);
+          qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g + 8) * KS + kk * 16 + 8 + 2 * tq);
+        }
+      }
+      if (active) {
+        const bf16* Ks = Kr + buf * KB * KS;
+        const bf16* Vs = Vr + buf * KB * KS;
+        const int k0 = kb * KB;
+        const int nj = min(KB, Tp - k0) / 8;   // n-tiles of 8 keys in this block (even: Tp % 16 == 0)
+        float s[KB / 8][4];
+#pragma unroll
+        for (int j = 0; j < KB / 8; ++j) {
+          s[j][0] = s[j][1] = s[j][2] = s[j][3] = -INFINITY;
+          if (j < nj) {
+            s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const bf16* kr = Ks + (j * 8 + g) * KS + kk * 16 + 2 * tq;
+              mma16816(s[j], qa[kk], *reinterpret_cast<const uint32_t*>(kr), *reinterpret_cast<const uint32_t*>(kr + 8));
+            }
+            const int col = k0 + j * 8 + 2 * tq;
+            if (col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
+            if (col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
+            if (qt == 0 && warp == 0 && g == 0) {   // raw logits of the CLS row (row 0)
+              scls[col] = s[j][0];
+              scls[col + 1] = s[j][1];
+            }
+          }
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < KB / 8; ++j) {
+          mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
+          mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float a0 = exp2f((m0 - mn0) * scale_log2), a1 = exp2f((m1 - mn1) * scale_log2);
+        const float ms0 = mn0 * scale_log2, ms1 = mn1 * scale_log2;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < KB / 8; ++j) {
+          s[j][0] = exp2f(fmaf(s[j][0], scale_log2, -ms0));
+          s[j][1] = exp2f(fmaf(s[j][1], scale_log2, -ms0));
+          s[j][2] = exp2f(fmaf(s[j][2], scale_log2, -ms1));
+          s[j][3] = exp2f(fmaf(s[j][3], scale_log2, -ms1));
+          rs0 += s[j][0] + s[j][1];
+          rs1 += s[j][2] + s[j][3];
+        }
+        l0 = l0 * a0 + rs0;
+        l1 = l1 * a1 + rs1;
+        m0 = mn0;
+        m1 = mn1;
+#pragma unroll
+        for (int i = 0; i < DH / 8; ++i) {
+          o[i][0] *= a0; o[i][1] *= a0; o[i][2] *= a1; o[i][3] *= a1;
+        }
+#pragma unroll
+        for (int kk = 0; kk < KB / 16; ++kk) {
+          if (2 * kk < nj) {
+            uint32_t pa[4];
+            pa[0] = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
+            pa[1] = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
+            pa[2] = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+            pa[3] = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+            for (int dt = 0; dt < DH / 8; dt += 2) {
+              // V fragments (row-major [key][dh]) via ldmatrix.trans: lanes 0-15 address keys
+              // 16kk+0..15 at column block dt, lanes 16-31 the same keys at block dt+1.
+              const bf16* vr = Vs + (kk * 16 + (lane & 15)) * KS + (dt + (lane >> 4)) * 8;
+              uint32_t b0, b1, b2, b3;
+              asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                           : "r"((uint32_t)__cvta_generic_to_shared(vr)));
+              mma16816(o[dt], pa, b0, b1);
+              mma16816(o[dt + 1], pa, b2, b3);
+            }
+          }
+        }
+      }
+      __syncthreads();   // ring slot `buf` is refilled by the next iteration's prefetch
     }
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int j = lane; j < T; j += 32) {
-      const float e = expf(ps[h * T + j] - mx);
-      ps[h * T + j] = e;
-      sum += e;
+    if (active) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+      const float il0 = 1.f / l0, il1 = 1.f / l1;
+      const int ra = qt * QT + r0 + g, rb = ra + 8;
+#pragma unroll
+      for (int dt = 0; dt < DH / 8; ++dt) {
+        const int col = h * DH + dt * 8 + 2 * tq;
+        if (ra < nq)
+          *reinterpret_cast<uint32_t*>(out + (long long)(q0 + ra) * D + col) = pack_bf16x2(o[dt][0] * il0, o[dt][1] * il0);
+        if (rb < nq)
+          *reinterpret_cast<uint32_t*>(out + (long long)(q0 + rb) * D + col) = pack_bf16x2(o[dt][2] * il1, o[dt][3] * il1);
+      }
+      if (qt == 0 && warp == 0 && lane == 0) { s_cls[0] = m0; s_cls[1] = l0; }
     }
-    sum = warp_sum(sum);
-    const float inv = 1.f / sum;
-    for (int j = lane; j < T; j += 32) ps[h * T + j] *= inv;
-  }
-  __syncthreads();
-  const int N = T - 1;
-  for (int j = 1 + threadIdx.x; j < T; j += blockDim.x) {
-    float acc = 0.f;
-    for (int hh = 0; hh < H; ++hh) acc += ps[hh * T + j];
-    pcls[(long long)slot * N + j - 1] = acc / (float)H;
+    if (qt == 0 && pclsh) {
+      // CLS softmax row of this head over the patch keys: p_j = exp2((s_j - m) scale) / l
+      __syncthreads();
+      const float mcls = s_cls[0], linv = 1.f / s_cls[1];
+      for (int j = 1 + tid; j < T; j += 128)
+        pclsh[((long long)slot * H + h) * (T - 1) + (j - 1)] = exp2f((scls[j] - mcls) * scale_log2) * linv;
+    }
   }
 }
 
 template <int DH>
-cudaError_t launch_attn_dh(const bf16* q, const bf16* KV, bf16* out, const int* wdesc, const int* qoff, int n_w,
-                           int T, int D, int H, cudaStream_t s) {
-  const int Tp = (T + KB - 1) / KB * KB;
-  const size_t smem = (size_t)(2 * Tp * (DH + 8) + QT * (DH + 8)) * sizeof(bf16);
+cudaError_t launch_attn_dh(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
+                           const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s) {
+  const int Tp = (T + 15) / 16 * 16;
+  const size_t smem = (size_t)(4 * KB * (DH + 8) + QT * (DH + 8)) * sizeof(bf16) + (size_t)Tp * 8;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  dim3 grid((T + QT - 1) / QT, H, n_w);
+  dim3 grid(H, n_w);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  attn_kernel<DH><<<grid, 128, smem, s>>>(q, KV, out, reinterpret_cast<const int4*>(wdesc), qoff, T, D, scale_log2);
+  attn_kernel<DH><<<grid, 128, smem, s>>>(q, KV, kvsrc, out, reinterpret_cast<const int4*>(wdesc), qoff, pclsh, T,
+                                          D, H, scale_log2);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_attention(const bf16* q, const bf16* KV, bf16* out, const int* wdesc, const int* qoff, int n_w,
-                             int T, int D, int H, cudaStream_t s) {
+cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
+                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
   const int dh = D / H;
-  if (dh == 64) return launch_attn_dh<64>(q, KV, out, wdesc, qoff, n_w, T, D, H, s);
-  if (dh == 16) return launch_attn_dh<16>(q, KV, out, wdesc, qoff, n_w, T, D, H, s);
+  if (dh == 64) return launch_attn_dh<64>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, s);
+  if (dh == 16) return launch_attn_dh<16>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, s);
   return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_cls_prob(const bf16* q, const bf16* KV, const int* wdesc, const int* qoff, float* pcls, int n_w,
-                            int T, int D, int H, cudaStream_t s) {
-  if (n_w <= 0) return cudaSuccess;
-  const int dh = D / H;
-  const size_t smem = (size_t)(H * dh + H * T) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(cls_prob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  cls_prob_kernel<<<n_w, 32 * H, smem, s>>>(q, KV, reinterpret_cast<const int4*>(wdesc), qoff, pcls, T, D, H, dh,
-                                            1.f / sqrtf((float)dh));
-  return cudaGetLastError();
 }
 
 }  // namespace rv

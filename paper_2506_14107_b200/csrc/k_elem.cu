@@ -61,8 +61,8 @@ __global__ void patch_to_bf16_kernel(const float* __restrict__ src, bf16* __rest
 template <int VPL>
 __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restrict__ cls,
                                     const float* __restrict__ pos, const float* __restrict__ g,
-                                    const float* __restrict__ b, float* __restrict__ pcls, int n,
-                                    int T, int D, int N) {
+                                    const float* __restrict__ b, float* __restrict__ pclsh, int n,
+                                    int T, int D, int N, int H) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long rows = (long long)n * T;
   for (long long r = blockIdx.x * (long long)ROWS_PER_CTA + warp; r < rows;
@@ -82,7 +82,7 @@ __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restri
       const int k = lane + 32 * j;
       if (k < D) row[k] = x[j];
     }
-    if (tok > 0 && lane == 0) pcls[(r / T) * N + (tok - 1)] = 1.0f / (float)N;  // layer-1 t
+    if (tok > 0 && lane < H) pclsh[((r / T) * H + lane) * N + (tok - 1)] = 1.0f / (float)N;  // layer-1 t
   }
 }
 
@@ -106,20 +106,25 @@ __global__ void gather_ln_kernel(const float* __restrict__ src, const int* __res
   }
 }
 
-__global__ void rgather_kernel(const float* __restrict__ X, bf16* __restrict__ KV,
-                               const int* __restrict__ idxR, const int* __restrict__ provrow,
-                               const int* __restrict__ count, bf16* __restrict__ Ar, int D) {
+// Delta R = X_{l-1}[row] - X_{l-1}[provrow] -> bf16 operand of the restoration layer (Eq. 8).
+__global__ void rgather_kernel(const float* __restrict__ X, const int* __restrict__ idxR,
+                               const int* __restrict__ provrow, const int* __restrict__ count,
+                               bf16* __restrict__ Ar, int D) {
   const int M = *count;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D4 = D >> 2;
   for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
-    const long long r = idxR[m], p = provrow[m];
-    const float* xr = X + r * D;
-    const float* xp = X + p * D;
-    bf16* o = Ar + (long long)m * D;
-    for (int k = lane; k < D; k += 32) o[k] = __float2bfloat16_rn(xr[k] - xp[k]);
-    const uint4* src = reinterpret_cast<const uint4*>(KV + p * 2 * D);
-    uint4* dst = reinterpret_cast<uint4*>(KV + r * 2 * D);
-    for (int k = lane; k < (2 * D) / 8; k += 32) dst[k] = src[k];
+    const float4* xr = reinterpret_cast<const float4*>(X + (long long)__ldg(idxR + m) * D);
+    const float4* xp = reinterpret_cast<const float4*>(X + (long long)__ldg(provrow + m) * D);
+    uint2* o = reinterpret_cast<uint2*>(Ar + (long long)m * D);
+#pragma unroll 4
+    for (int k = lane; k < D4; k += 32) {
+      const float4 a = __ldg(xr + k), b = __ldg(xp + k);
+      uint2 u;
+      u.x = pack_bf16x2(a.x - b.x, a.y - b.y);
+      u.y = pack_bf16x2(a.z - b.z, a.w - b.w);
+      o[k] = u;
+    }
   }
 }
 
@@ -158,12 +163,12 @@ cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, in
 }
 
 cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g,
-                                const float* b, float* pcls, int n, int T, int D, int N, cudaStream_t s) {
+                                const float* b, float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s) {
   const int grid = grid_rows((long long)n * T);
   const int v = (D + 31) / 32;
-  if (v <= 2) embed_finish_kernel<2><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
-  else if (v <= 24) embed_finish_kernel<24><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
-  else embed_finish_kernel<32><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pcls, n, T, D, N);
+  if (v <= 2) embed_finish_kernel<2><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
+  else if (v <= 24) embed_finish_kernel<24><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
+  else embed_finish_kernel<32><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
   return cudaGetLastError();
 }
 
@@ -177,9 +182,9 @@ cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count
   return cudaGetLastError();
 }
 
-cudaError_t launch_rgather(const float* X, bf16* KV, const int* idxR, const int* provrow, const int* count,
-                           int max_rows, bf16* Ar, int D, cudaStream_t s) {
-  rgather_kernel<<<grid_rows(max_rows), 256, 0, s>>>(X, KV, idxR, provrow, count, Ar, D);
+cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
+                           bf16* Ar, int D, cudaStream_t s) {
+  rgather_kernel<<<grid_rows(max_rows), 256, 0, s>>>(X, idxR, provrow, count, Ar, D);
   return cudaGetLastError();
 }
 

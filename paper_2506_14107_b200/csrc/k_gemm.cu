@@ -7,12 +7,13 @@
 // no host synchronisation is needed between compaction and the contractions
 // and the whole layer loop is CUDA-graph capturable.
 //
-// CTA = 256 threads, one CTA per SM (persistent over 128 x BN output tiles):
+// CTA = 320 threads, one CTA per SM (persistent over 128 x BN output tiles):
 //   warp 0 : TMA producer (one elected lane), STAGES-deep smem ring, SWIZZLE_128B tiles
 //   warp 1 : MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
-//   warp 2 : TMEM allocator (2*BN fp32 columns: double-buffered accumulator)
-//   warps 4-7 : epilogue, tcgen05.ld 32x32b.x32 -> bias / QuickGELU / residual -> row-mapped
-//               (scatter) stores in fp32 or bf16
+//   warp 1 also allocates TMEM (2*BN fp32 columns: double-buffered accumulator)
+//   warps 2-9 : epilogue (warp%4 = TMEM lane quarter, (warp-2)/4 = column half):
+//               tcgen05.ld 32x32b.x32 -> smem transpose -> coalesced bias / QuickGELU /
+//               residual / row-mapped (scatter) stores in fp32 or bf16
 // Fixed tiles and no split-K: every output element is accumulated in the same K order
 // regardless of M or of its row position, so results are batch-invariant.
 #include <cuda.h>
@@ -28,7 +29,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;            // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 320;   // TMA warp + MMA/TMEM warp + 8 epilogue warps
+constexpr int EPI_WARPS = 8;
 
 template <int BN>
 struct Cfg {
@@ -37,7 +39,9 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int STAGE_OUT = EPI_WARPS * (32 * 32 + 64) * 4;   // per-warp 32x32 fp32 transpose tile + row maps
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT + 256 /*barriers*/;
+  static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
 RV_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -77,6 +81,14 @@ RV_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
 }
 RV_DEV void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+RV_DEV void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+RV_DEV float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
 }
 RV_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 RV_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -120,65 +132,12 @@ RV_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Epilogue for one row m and 32 consecutive columns n0..n0+31 (fp32 accumulators in r).
-RV_DEV void epilogue_32(const Epi& e, int m, int n0, const uint32_t (&r)[32]) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-  if (e.bias) {
-    const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 b = __ldg(b4 + j);
-      v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
-    }
-  }
-  if (e.act == 1) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = quick_gelu(v[j]);
-  }
-  if (e.resid) {
-    const long long rr = e.resid_rows ? (long long)e.resid_rows[m] : (long long)m;
-    const float4* p4 = reinterpret_cast<const float4*>(e.resid + rr * e.resid_ld + n0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 x = p4[j];
-      v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
-    }
-  }
-  void* base;
-  long long row, ld;
-  int col, as_bf16;
-  if (n0 >= e.split) {
-    base = e.out2;
-    row = e.out2_rows ? (long long)e.out2_rows[m] : (long long)m;
-    ld = e.out2_ld;
-    col = n0 - e.split;
-    as_bf16 = e.out2_bf16;
-  } else {
-    base = e.out;
-    row = e.out_rows ? (long long)e.out_rows[m]
-                     : (long long)m + (e.row_div ? m / e.row_div : 0) + e.row_add;
-    ld = e.out_ld;
-    col = n0;
-    as_bf16 = e.out_bf16;
-  }
-  if (as_bf16) {
-    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(base) + row * ld + col);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint4 u;
-      u.x = pack_bf16x2(v[8 * j + 0], v[8 * j + 1]);
-      u.y = pack_bf16x2(v[8 * j + 2], v[8 * j + 3]);
-      u.z = pack_bf16x2(v[8 * j + 4], v[8 * j + 5]);
-      u.w = pack_bf16x2(v[8 * j + 6], v[8 * j + 7]);
-      o[j] = u;
-    }
-  } else {
-    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + row * ld + col);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  }
+// QuickGELU for the GEMM epilogue: x * sigmoid(1.702 x) = x * (0.5 + 0.5 tanh(0.851 x)), one
+// MUFU.TANH per element (tanh.approx, rel. err ~2^-11; the result is rounded to bf16).
+RV_DEV float quick_gelu_fast(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.851f * x));
+  return x * fmaf(0.5f, t, 0.5f);
 }
 
 template <int BN>
@@ -186,11 +145,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
   using C = Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];   // SWIZZLE_128B needs 1024-B aligned stages
+  uint8_t* smem = smem_raw;
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  float* sOut = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sOut) + C::STAGE_OUT);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -211,11 +171,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], EPI_WARPS * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -266,21 +226,102 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mma_commit(&tfull[acc]);              // accumulator ready for the epilogue
       }
     }
-  } else if (warp >= 4) {
-    const int q = warp - 4;                   // TMEM lanes 32q .. 32q+31 (warp % 4 == q)
+  } else if (warp >= 2) {
+    // 8 epilogue warps: warp%4 selects the TMEM lane quarter (rows 32q..32q+31), (warp-4)/4
+    // selects the column half.  Per 32-column chunk: tcgen05.ld (thread = row) -> rotated
+    // st.shared (conflict-free) -> row-wise ld.shared (8 lanes per row, 4 rows per warp
+    // access) -> bias / QuickGELU / residual / row-mapped store, all coalesced.  Row maps are
+    // loaded once per tile and the 8 residual loads of a chunk are issued together (MLP).
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    float* tile_s = sOut + (warp - 2) * (32 * 32 + 64);
+    int* orow_s = reinterpret_cast<int*>(tile_s + 32 * 32);   // [32] output row of each tile row
+    int* rrow_s = orow_s + 32;                                  // [32] residual row
+    const uint32_t tile_u = smem_u32(tile_s);
+    const int rsub = lane >> 3;          // row within a group of 4
+    const int c4 = (lane & 7) * 4;       // first of this lane's 4 columns
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int mb = tile / tiles_n, nb = tile % tiles_n;
+      const int row0 = mb * BM + q * 32;
+      // per-tile row maps (lane = row within this warp's 32 rows), kept in shared memory
+      {
+        const int m = row0 + lane;
+        const int mm = m < M ? m : 0;
+        orow_s[lane] = e.out_rows ? __ldg(e.out_rows + mm) : mm + (e.row_div ? mm / e.row_div : 0) + e.row_add;
+        rrow_s[lane] = e.resid ? (e.resid_rows ? __ldg(e.resid_rows + mm) : mm) : 0;
+      }
+      const int nvalid = min(32, M - row0);     // rows of this warp that exist (may be <= 0)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int m = mb * BM + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
-        if (m < M) epilogue_32(e, m, nb * BN + c * 32, r);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4)   // 16-B chunk j4 of row `lane` at chunk slot j4 ^ (lane & 7)
+          sts128(tile_u + lane * 128 + ((j4 ^ (lane & 7)) << 4), r[4 * j4], r[4 * j4 + 1], r[4 * j4 + 2], r[4 * j4 + 3]);
+        __syncwarp();
+        const int n0 = nb * BN + c * 32 + c4;
+        const bool second = n0 >= e.split;
+        void* base = second ? e.out2 : e.out;
+        const long long ld = second ? e.out2_ld : e.out_ld;
+        const int col = second ? n0 - e.split : n0;
+        const bool obf16 = second ? e.out2_bf16 : e.out_bf16;
+        float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e.bias) b = __ldg(reinterpret_cast<const float4*>(e.bias + n0));
+#pragma unroll
+        for (int ih = 0; ih < 2; ++ih) {      // two passes of 4 rows: 4 residual loads in flight
+          float4 v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int rr = (ih * 4 + k) * 4 + rsub;
+            const float4 t4 = lds128(tile_u + rr * 128 + (((lane & 7) ^ (rr & 7)) << 4));
+            v[k].x = t4.x + b.x;
+            v[k].y = t4.y + b.y;
+            v[k].z = t4.z + b.z;
+            v[k].w = t4.w + b.w;
+          }
+          if (e.act == 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              v[k].x = quick_gelu_fast(v[k].x); v[k].y = quick_gelu_fast(v[k].y);
+              v[k].z = quick_gelu_fast(v[k].z); v[k].w = quick_gelu_fast(v[k].w);
+            }
+          }
+          if (e.resid) {
+            float4 x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = ih * 4 + k;
+              const int rr = i * 4 + rsub;
+              x[k] = rr < nvalid ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld + n0)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { v[k].x += x[k].x; v[k].y += x[k].y; v[k].z += x[k].z; v[k].w += x[k].w; }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = ih * 4 + k;
+            const int rr = i * 4 + rsub;
+            if (rr >= nvalid) continue;
+            const int m = row0 + rr;
+            const int orr = second ? (e.out2_rows ? __ldg(e.out2_rows + m) : m) : orow_s[rr];
+            const long long off = (long long)orr * ld + col;
+            if (obf16) {
+              uint2 u;
+              u.x = pack_bf16x2(v[k].x, v[k].y);
+              u.y = pack_bf16x2(v[k].z, v[k].w);
+              *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(base) + off) = u;
+            } else {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = v[k];
+            }
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -288,7 +329,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
   }

@@ -19,58 +19,71 @@ namespace rv {
 namespace {
 
 constexpr int SCORE_THREADS = 256;
+constexpr int SCORE_TOK = 32;      // tokens per CTA (8 warps x 4 tokens): grid = n_w x ceil(N/32)
 
 __global__ void __launch_bounds__(SCORE_THREADS)
     score_kernel(const float* __restrict__ X, int T, int D, int N, int L, int layer,
-                 const int4* __restrict__ wdesc, const float* __restrict__ tfeat,
+                 const int4* __restrict__ wdesc, const float* __restrict__ tsrc, int tH,
                  const float* __restrict__ codec, const uint8_t* force,
                  const float* __restrict__ gate, int Hg, int dense, uint8_t* masks, float* scores,
-                 uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntC) {
+                 uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntR) {
   __shared__ int s_reused;
   const int w = blockIdx.x;
+  const int i_beg = 1 + blockIdx.y * SCORE_TOK;
+  const int i_end = min(N, i_beg + SCORE_TOK - 1);
   const int4 d4 = wdesc[w];
   const int slot = d4.x, past = d4.y, fut = d4.z, type = d4.w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = SCORE_THREADS / 32;
-  if (threadIdx.x == 0) s_reused = 0;
   const long long mrow = ((long long)slot * L + layer) * N;   // masks/scores row of (slot, layer)
   const bool no_decision = dense || type == 0 || (past < 0 && fut < 0);
   if (threadIdx.x == 0) {
-    wmask[(long long)w * T] = 0;
-    wprov[(long long)w * T] = 0;
+    s_reused = 0;
+    if (blockIdx.y == 0) {
+      wmask[(long long)w * T] = 0;
+      wprov[(long long)w * T] = 0;
+    }
   }
   if (no_decision) {
-    for (int i = 1 + threadIdx.x; i <= N; i += SCORE_THREADS) {
+    for (int i = i_beg + threadIdx.x; i <= i_end; i += SCORE_THREADS) {
       wmask[(long long)w * T + i] = 0;
       wprov[(long long)w * T + i] = 0;
       if (masks) masks[mrow + i - 1] = 0;
       if (scores) scores[mrow + i - 1] = __int_as_float(0x7fc00000);   // NaN: no decision ran
     }
-    if (threadIdx.x == 0) cntC[w] = T;
     return;
   }
   __syncthreads();
   // Decision-MLP weights of this layer: Wd1[7][Hg], bd1[Hg], Wd2[Hg], bd2[1].
   float w1[7], b1 = 0.f, w2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < 7; ++k) w1[k] = lane < Hg ? gate[k * Hg + lane] : 0.f;
+  for (int k = 0; k < 7; ++k) w1[k] = lane < Hg ? __ldg(gate + k * Hg + lane) : 0.f;
   if (lane < Hg) {
-    b1 = gate[7 * Hg + lane];
-    w2 = gate[8 * Hg + lane];
+    b1 = __ldg(gate + 7 * Hg + lane);
+    w2 = __ldg(gate + 8 * Hg + lane);
   }
-  const float b2 = gate[9 * Hg];
+  const float b2 = __ldg(gate + 9 * Hg);
   const float oh0 = type == 0, oh1 = type == 1, oh2 = type == 2, oh3 = type == 3;
+  const int D4 = D >> 2;
   int my_reused = 0;
-  for (int i = 1 + warp; i <= N; i += nwarps) {
-    const float* cur = X + ((long long)slot * T + i) * D;
-    const float* rp = past >= 0 ? X + ((long long)past * T + i) * D : nullptr;
-    const float* rf = fut >= 0 ? X + ((long long)fut * T + i) * D : nullptr;
+  for (int i = i_beg + warp; i <= i_end; i += SCORE_THREADS / 32) {
+    const float4* cur = reinterpret_cast<const float4*>(X + ((long long)slot * T + i) * D);
+    const float4* rp = past >= 0 ? reinterpret_cast<const float4*>(X + ((long long)past * T + i) * D) : nullptr;
+    const float4* rf = fut >= 0 ? reinterpret_cast<const float4*>(X + ((long long)fut * T + i) * D) : nullptr;
     float cc = 0.f, pp = 0.f, ff = 0.f, cp = 0.f, cf = 0.f;
-    for (int k = lane; k < D; k += 32) {
-      const float c = cur[k];
-      cc += c * c;
-      if (rp) { const float p = rp[k]; pp += p * p; cp += c * p; }
-      if (rf) { const float f = rf[k]; ff += f * f; cf += c * f; }
+#pragma unroll 4
+    for (int k = lane; k < D4; k += 32) {
+      const float4 c = __ldg(cur + k);
+      cc += c.x * c.x + c.y * c.y + c.z * c.z + c.w * c.w;
+      if (rp) {
+        const float4 p = __ldg(rp + k);
+        pp += p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w;
+        cp += c.x * p.x + c.y * p.y + c.z * p.z + c.w * p.w;
+      }
+      if (rf) {
+        const float4 f = __ldg(rf + k);
+        ff += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+        cf += c.x * f.x + c.y * f.y + c.z * f.z + c.w * f.w;
+      }
     }
     cc = warp_sum(cc);
     pp = warp_sum(pp);
@@ -88,8 +101,11 @@ __global__ void __launch_bounds__(SCORE_THREADS)
       const float sf = den > 0.f ? cf / den : 0.f;
       if (sf > s) { s = sf; prov = 1; }   // strict: ties keep the past reference
     }
-    const float t = tfeat[(long long)slot * N + i - 1];
-    const float c = codec[(long long)slot * N + i - 1];
+    // t_i = head-mean of the previous layer's CLS attention to token i (fixed order)
+    float t = 0.f;
+    for (int hh = 0; hh < tH; ++hh) t += __ldg(tsrc + ((long long)slot * tH + hh) * N + i - 1);
+    t = t / (float)tH;
+    const float c = __ldg(codec + (long long)slot * N + i - 1);
     float h = b1 + s * w1[0] + t * w1[1] + oh0 * w1[2] + oh1 * w1[3] + oh2 * w1[4] + oh3 * w1[5] + c * w1[6];
     h = lane < Hg ? quick_gelu(h) * w2 : 0.f;
     const float dlogit = warp_sum(h) + b2;
@@ -105,16 +121,16 @@ __global__ void __launch_bounds__(SCORE_THREADS)
   }
   if (lane == 0 && my_reused) atomicAdd(&s_reused, my_reused);
   __syncthreads();
-  if (threadIdx.x == 0) cntC[w] = T - s_reused;
+  if (threadIdx.x == 0 && s_reused) atomicAdd(cntR + w, s_reused);   // integer: order-independent
 }
 
 constexpr int COMPACT_THREADS = 256;
 
 __global__ void __launch_bounds__(COMPACT_THREADS)
     compact_kernel(int n_w, int T, const int4* __restrict__ wdesc, const uint8_t* __restrict__ wmask,
-                   const uint8_t* __restrict__ wprov, const int* __restrict__ cntC, int* __restrict__ idxC,
+                   const uint8_t* __restrict__ wprov, const int* __restrict__ cntR, int* __restrict__ idxC,
                    int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
-                   int* __restrict__ counts, unsigned long long* reuse_ctr, int* count_log) {
+                   int* __restrict__ counts, int* kvsrc, unsigned long long* reuse_ctr, int* count_log) {
   __shared__ int s_part[COMPACT_THREADS / 32];
   __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
   __shared__ int s_base[2];
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // offC = sum_{v<w} |C_v| (exact integer reduction)
   int part = 0;
-  for (int v = threadIdx.x; v < w; v += COMPACT_THREADS) part += cntC[v];
+  for (int v = threadIdx.x; v < w; v += COMPACT_THREADS) part += T - cntR[v];
   part = warp_sum_i(part);
   if (lane == 0) s_part[warp] = part;
   __syncthreads();
@@ -133,7 +149,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
     s_base[1] = w * T - off;         // R offset (|R_v| = T - |C_v|)
     qoff[w] = off;
     if (w == n_w - 1) {
-      const int tot = off + cntC[w];
+      const int tot = off + T - cntR[w];
       qoff[n_w] = tot;
       counts[0] = tot;
       counts[1] = n_w * T - tot;
@@ -163,11 +179,18 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
       tr += s_wr[k];
     }
     const unsigned lt = (1u << lane) - 1u;
-    if (isC) idxC[offC + pc + __popc(bc & lt)] = slot * T + i;
+    if (isC) {
+      idxC[offC + pc + __popc(bc & lt)] = slot * T + i;
+      if (kvsrc) kvsrc[(long long)slot * T + i] = slot * T + i;
+    }
     if (isR) {
       const int r = offR + pr + __popc(br & lt);
+      const int prow = (pv[i] ? d4.z : d4.y) * T + i;
       idxR[r] = slot * T + i;
-      provrow[r] = (pv[i] ? d4.z : d4.y) * T + i;
+      provrow[r] = prow;
+      // reuse-cache read in place: K/V of a reused token = its provider's (already final,
+      // the provider ran in an earlier level), chains resolved here (one hop at read time)
+      if (kvsrc) kvsrc[(long long)slot * T + i] = kvsrc[prow];
     }
     offC += tc;
     offR += tr;
@@ -178,21 +201,24 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
 }  // namespace
 
 cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
-                         const float* tfeat, const float* codec, const uint8_t* force, const float* gate,
+                         const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
-                         int* cntC, cudaStream_t s) {
+                         int* cntR, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
-  score_kernel<<<n_w, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, reinterpret_cast<const int4*>(wdesc), tfeat,
-                                             codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntC);
+  cudaError_t e = cudaMemsetAsync(cntR, 0, (size_t)n_w * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  dim3 grid(n_w, (N + SCORE_TOK - 1) / SCORE_TOK);
+  score_kernel<<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, reinterpret_cast<const int4*>(wdesc), tsrc, tH,
+                                              codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntR);
   return cudaGetLastError();
 }
 
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
-                           const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
+                           const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
                            unsigned long long* reuse_ctr, int* count_log, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
   compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
-                                                 cntC, idxC, idxR, provrow, qoff, counts, reuse_ctr, count_log);
+                                                 cntR, idxC, idxR, provrow, qoff, counts, kvsrc, reuse_ctr, count_log);
   return cudaGetLastError();
 }
 

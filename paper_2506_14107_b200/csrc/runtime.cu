@@ -67,14 +67,15 @@ struct rv_ctx {
   std::vector<void*> ballocs;
   float* X[2] = {nullptr, nullptr};
   bf16* KV = nullptr;
-  float* pcls = nullptr;
+  float* pclsh = nullptr;     // [n][H][N] per-head CLS attention of the previous layer (t)
+  int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
   bf16* patches_bf16 = nullptr;
   float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
   uint8_t* out_masks = nullptr;
   int* wdesc = nullptr;
   int wdesc_cap = 0;
   uint8_t *wmask = nullptr, *wprov = nullptr;
-  int *cntC = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr;
+  int *cntR = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr;
   bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *Ar = nullptr, *hr = nullptr;
   float* x1 = nullptr;
   unsigned long long* reuse_ctr = nullptr;   // [L]
@@ -141,7 +142,7 @@ bool cfg_valid(const rv_config* c, char* why, size_t n) {
   if (c->heads > 32) { snprintf(why, n, "heads must be <= 32"); return false; }
   if (c->patch < 1 || c->img < c->patch || c->img % c->patch) { snprintf(why, n, "img must be a positive multiple of patch"); return false; }
   const int N = (c->img / c->patch) * (c->img / c->patch);
-  if (N + 1 > 1024) { snprintf(why, n, "T = N+1 must be <= 1024"); return false; }
+  if (N + 1 > 768) { snprintf(why, n, "T = N+1 must be <= 768 (attention keeps a frame's K/V in smem)"); return false; }
   if (c->ffn < 64 || c->ffn % 64) { snprintf(why, n, "ffn must be a positive multiple of 64"); return false; }
   if (c->hidden_r < 64 || c->hidden_r % 64) { snprintf(why, n, "hidden_r must be a positive multiple of 64"); return false; }
   if (c->hidden_g < 1 || c->hidden_g > 32) { snprintf(why, n, "hidden_g must be 1..32"); return false; }
@@ -263,7 +264,8 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->X[0], n * T * D);
   AL(ctx->X[1], n * T * D);
   AL(ctx->KV, n * T * 2 * D);
-  AL(ctx->pcls, n * N);
+  AL(ctx->pclsh, n * ctx->H * N);
+  AL(ctx->kvsrc, n * T);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
   AL(ctx->in_patches, (size_t)n * N * ctx->pp);
   AL(ctx->in_codec, n * N);
@@ -273,7 +275,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->wdesc, (size_t)n * 4);
   AL(ctx->wmask, max_w * T);
   AL(ctx->wprov, max_w * T);
-  AL(ctx->cntC, max_w);
+  AL(ctx->cntR, max_w);
   AL(ctx->qoff, max_w + 1);
   AL(ctx->counts, 2);
   AL(ctx->idxC, capC);
@@ -364,7 +366,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
     r.chk(gemm_launch(ctx->pe, nullptr, n * N, n * N, e, s), "gemm_pe");
   }
   r.begin(K_EMBED,-1,-1);
-  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pcls, n, T, D, N, s),
+  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
         "embed_finish");
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
@@ -377,14 +379,14 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       const int maxC = n_w * T, maxR = n_w * N;
       // a2-a3: Eq. 1-4
       r.begin(K_SCORE,l,wi);
-      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pcls, codec, force ? masks : nullptr,
+      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
                          ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
-                         ctx->wprov, ctx->cntC, s),
+                         ctx->wprov, ctx->cntR, s),
             "score");
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
-      r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntC, ctx->idxC, ctx->idxR, ctx->provrow,
-                           ctx->qoff, ctx->counts, ctx->reuse_ctr + l,
+      r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
+                           ctx->qoff, ctx->counts, ctx->kvsrc, ctx->reuse_ctr + l,
                            ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, s),
             "compact");
       const int* MC = ctx->counts;
@@ -408,11 +410,12 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
       }
       // a7 + Eq. 8: reused rows take the provider's K/V; Delta for the restoration layer
-      if (wv.any_ref) { r.begin(K_RGATHER,l,wi); r.chk(launch_rgather(Xin, ctx->KV, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather"); }
+      if (wv.any_ref) { r.begin(K_RGATHER,l,wi); r.chk(launch_rgather(Xin, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather"); }
       // a8: attention over all T keys; CLS row -> t for layer l+1
       r.begin(K_ATTN,l,wi);
-      r.chk(launch_attention(ctx->q, ctx->KV, ctx->att, wd, ctx->qoff, n_w, T, D, H, s), "attention");
-      if (!dense && l + 1 < L) { r.begin(K_CLS,l,wi); r.chk(launch_cls_prob(ctx->q, ctx->KV, wd, ctx->qoff, ctx->pcls, n_w, T, D, H, s), "cls_prob"); }
+      r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff,
+                             (!dense && l + 1 < L) ? ctx->pclsh : nullptr, n_w, T, D, H, s),
+            "attention");
       // a9: W_o + residual (gathered X_{l-1} rows)
       {
         Epi e;
@@ -931,22 +934,22 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
 // ---------------------------------------------------------------------- stage entry points
 rv_status rv_stage_score(rv_ctx* ctx, int32_t layer, const float* X, int32_t n_w, const int32_t* wdesc,
                          const float* t, const float* codec, const uint8_t* force, uint8_t* masks, float* scores,
-                         uint8_t* wmask, uint8_t* wprov, int32_t* cntC, void* stream) {
+                         uint8_t* wmask, uint8_t* wprov, int32_t* cntR, void* stream) {
   if (!ctx) return RV_ECONTRACT;
   if (!ctx->gates_loaded) return fail(ctx, RV_ECONTRACT, "rv_stage_score: gates not loaded");
   if (layer < 0 || layer >= ctx->L || n_w < 0) return fail(ctx, RV_ECONTRACT, "rv_stage_score: bad layer/n_w");
   CK(cudaSetDevice(ctx->device));
-  CK(launch_score(X, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, codec, force, ctx->lw[layer].gate,
-                  ctx->Hg, 0, masks, scores, wmask, wprov, cntC, (cudaStream_t)stream));
+  CK(launch_score(X, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, 1, codec, force, ctx->lw[layer].gate,
+                  ctx->Hg, 0, masks, scores, wmask, wprov, cntR, (cudaStream_t)stream));
   return RV_OK;
 }
 
 rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const uint8_t* wmask,
-                           const uint8_t* wprov, const int32_t* cntC, int32_t* idxC, int32_t* idxR,
+                           const uint8_t* wprov, const int32_t* cntR, int32_t* idxC, int32_t* idxR,
                            int32_t* provrow, int32_t* qoff, int32_t* counts, void* stream) {
   if (!ctx) return RV_ECONTRACT;
   CK(cudaSetDevice(ctx->device));
-  CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntC, idxC, idxR, provrow, qoff, counts, nullptr, nullptr,
+  CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntR, idxC, idxR, provrow, qoff, counts, nullptr, nullptr, nullptr,
                     (cudaStream_t)stream));
   return RV_OK;
 }
@@ -974,11 +977,8 @@ rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, con
                              const void* KV, void* out, float* pcls, void* stream) {
   if (!ctx) return RV_ECONTRACT;
   CK(cudaSetDevice(ctx->device));
-  CK(launch_attention((const bf16*)q, (const bf16*)KV, (bf16*)out, wdesc, qoff, n_w, ctx->T, ctx->D, ctx->H,
-                      (cudaStream_t)stream));
-  if (pcls)
-    CK(launch_cls_prob((const bf16*)q, (const bf16*)KV, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
-                       (cudaStream_t)stream));
+  CK(launch_attention((const bf16*)q, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D,
+                      ctx->H, (cudaStream_t)stream));
   return RV_OK;
 }
 

@@ -49,27 +49,24 @@ cudaError_t gemm_launch(const GemmPlan& p, const int* M_dev, int M_host, int max
 typedef __nv_bfloat16 bf16;
 cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP, cudaStream_t s);
 cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g, const float* b,
-                                float* pcls, int n, int T, int D, int N, cudaStream_t s);
+                                float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s);
 cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
                              const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
-cudaError_t launch_rgather(const float* X, bf16* KV, const int* idxR, const int* provrow, const int* count,
-                           int max_rows, bf16* Ar, int D, cudaStream_t s);
+cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
+                           bf16* Ar, int D, cudaStream_t s);
 cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
                            cudaStream_t s);
 
 // ---------------------------------------------------------------- decision + compaction (k_score.cu)
 cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
-                         const float* tfeat, const float* codec, const uint8_t* force, const float* gate,
+                         const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
-                         int* cntC, cudaStream_t s);
+                         int* cntR, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
-                           const int* cntC, int* idxC, int* idxR, int* provrow, int* qoff, int* counts,
+                           const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
                            unsigned long long* reuse_ctr, int* count_log, cudaStream_t s);
 
 // ---------------------------------------------------------------- attention (k_attn.cu)
-cudaError_t launch_attention(const bf16* q, const bf16* KV, bf16* out, const int* wdesc, const int* qoff, int n_w,
-                             int T, int D, int H, cudaStream_t s);
-cudaError_t launch_cls_prob(const bf16* q, const bf16* KV, const int* wdesc, const int* qoff, float* pcls, int n_w,
-                            int T, int D, int H, cudaStream_t s);
+cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
+                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s);
 }  // namespace rv
-

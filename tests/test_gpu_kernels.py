@@ -87,7 +87,7 @@ def test_attention_vs_torch(dev, cfgname):
     wdesc = np.zeros((n_w, 4), np.int32)
     wdesc[:, 0] = slot_of
     out = torch.zeros((qoff[-1], D), dtype=torch.bfloat16, device=dev)
-    pcls = torch.zeros((slots, cfg.N), dtype=torch.float32, device=dev)
+    pcls = torch.zeros((slots, H, cfg.N), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
     m.stage_attention(torch.from_numpy(wdesc).to(dev), torch.from_numpy(qoff).to(dev), q.to(dev), KV.to(dev),
                       out, pcls, st)
@@ -101,7 +101,7 @@ def test_attention_vs_torch(dev, cfgname):
         ref = (P @ Vf).transpose(0, 1).reshape(-1, D)
         got = out[qoff[w]:qoff[w + 1]].cpu().float()
         assert (got - ref).abs().max().item() < 2e-2 * (1 + ref.abs().max().item())
-        tref = P[:, 0, 1:].mean(0)
+        tref = P[:, 0, 1:]                       # per-head CLS softmax row over patch keys
         assert (pcls[s].cpu() - tref).abs().max().item() < 1e-4
 
 
@@ -128,9 +128,9 @@ def test_score_teacher_forced(dev, cfgname, mode, n):
         scores = torch.zeros((n, L, N), dtype=torch.float32, device=dev)
         wmask = torch.zeros((len(frames), T), dtype=torch.uint8, device=dev)
         wprov = torch.zeros_like(wmask)
-        cntC = torch.zeros(len(frames), dtype=torch.int32, device=dev)
+        cntR = torch.zeros(len(frames), dtype=torch.int32, device=dev)
         m.stage_score(l, Xd, torch.from_numpy(wdesc).to(dev), torch.from_numpy(t).to(dev),
-                      torch.from_numpy(c).to(dev), None, masks, scores, wmask, wprov, cntC, st)
+                      torch.from_numpy(c).to(dev), None, masks, scores, wmask, wprov, cntR, st)
         torch.cuda.synchronize()
         d_ref = ref["d"][:, l, :]
         d_gpu = scores[:, l, :].cpu().double().numpy()
@@ -141,7 +141,7 @@ def test_score_teacher_forced(dev, cfgname, mode, n):
             checked += band.sum()
         wm = wmask.cpu().numpy()
         assert np.all(wm[:, 0] == 0)
-        assert np.array_equal(cntC.cpu().numpy(), T - wm.sum(1))
+        assert np.array_equal(cntR.cpu().numpy(), wm.sum(1))
     assert checked > 0
 
 
@@ -161,14 +161,14 @@ def test_compaction_bitexact(dev, n_w, p):
     past = rng.integers(0, 50, n_w).astype(np.int32)
     fut = rng.integers(0, 50, n_w).astype(np.int32)
     wdesc = np.stack([slots, past, fut, np.ones(n_w, np.int32)], 1).astype(np.int32)
-    cntC = (T - masks.sum(1)).astype(np.int32)
+    cntR = masks.sum(1).astype(np.int32)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     idxC = torch.full((n_w * T,), -1, dtype=torch.int32, device=dev)
     idxR = torch.full((n_w * T,), -1, dtype=torch.int32, device=dev)
     provrow = torch.full((n_w * T,), -1, dtype=torch.int32, device=dev)
     qoff = torch.zeros(n_w + 1, dtype=torch.int32, device=dev)
     counts = torch.zeros(2, dtype=torch.int32, device=dev)
-    m.stage_compact(d(wdesc), d(masks), d(prov), d(cntC), idxC, idxR, provrow, qoff, counts,
+    m.stage_compact(d(wdesc), d(masks), d(prov), d(cntR), idxC, idxR, provrow, qoff, counts,
                     torch.cuda.current_stream())
     torch.cuda.synchronize()
     eC, eR, eq = oracle.compaction_indices(masks)
