@@ -110,18 +110,6 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def shard(n_total, refresh, rank, world):
-    """Contiguous runs of refresh groups per rank + the right-edge I-frame as a halo
-    (SURVEY D9): returns (first display frame, owned frames, frames computed incl. halo)."""
-    groups = (n_total + refresh - 1) // refresh
-    g0 = groups * rank // world
-    g1 = groups * (rank + 1) // world
-    f0 = g0 * refresh
-    f1 = min(n_total, g1 * refresh)
-    halo = 1 if f1 < n_total else 0
-    return f0, f1 - f0, f1 - f0 + halo
-
-
 def torch_dense_fps(cfg, W, x_dev, batch=256):
     """Dense torch ViT on the same GPU (cuBLAS bf16 matmul + SDPA, fp32 residual): baseline (i)."""
     import torch
@@ -232,6 +220,7 @@ def main():
 
     import synth
     from paper_2506_14107_b200 import ReuseViT, plan_gop
+    from paper_2506_14107_b200.dist import shard_frames as shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -23,7 +23,7 @@ constexpr int QT = 64;   // query rows per q-tile (4 warps x 16)
 constexpr int KB = 64;   // keys per online-softmax block / cp.async commit group
 
 RV_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
@@ -127,22 +127,32 @@ __global__ void __launch_bounds__(128)
         const int nj = min(KB, Tp - k0) / 8;   // n-tiles of 8 keys in this block (even: Tp % 16 == 0)
         float s[KB / 8][4];
 #pragma unroll
-        for (int j = 0; j < KB / 8; ++j) {
-          s[j][0] = s[j][1] = s[j][2] = s[j][3] = -INFINITY;
-          if (j < nj) {
-            s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        for (int j = 0; j < KB / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        // S = Q K^T: kk outer so the 8 n-tile accumulators are independent; K fragments of two
+        // n-tiles per ldmatrix.x4 (rows = keys, non-transposed)
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {
-              const bf16* kr = Ks + (j * 8 + g) * KS + kk * 16 + 2 * tq;
-              mma16816(s[j], qa[kk], *reinterpret_cast<const uint32_t*>(kr), *reinterpret_cast<const uint32_t*>(kr + 8));
+        for (int kk = 0; kk < DH / 16; ++kk) {
+#pragma unroll
+          for (int j = 0; j < KB / 8; j += 2) {
+            if (j < nj) {
+              const bf16* kr = Ks + (j * 8 + (lane & 7) + ((lane >> 4) << 3)) * KS + kk * 16 + ((lane >> 3) & 1) * 8;
+              uint32_t b0, b1, b2, b3;
+              asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                           : "r"((uint32_t)__cvta_generic_to_shared(kr)));
+              mma16816(s[j], qa[kk], b0, b1);
+              mma16816(s[j + 1], qa[kk], b2, b3);
             }
-            const int col = k0 + j * 8 + 2 * tq;
-            if (col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
-            if (col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
-            if (qt == 0 && warp == 0 && g == 0) {   // raw logits of the CLS row (row 0)
-              scls[col] = s[j][0];
-              scls[col + 1] = s[j][1];
-            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < KB / 8; ++j) {
+          const int col = k0 + j * 8 + 2 * tq;
+          if (j >= nj || col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
+          if (j >= nj || col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
+          if (qt == 0 && warp == 0 && g == 0 && j < nj) {   // raw logits of the CLS row (row 0)
+            scls[col] = s[j][0];
+            scls[col + 1] = s[j][1];
           }
         }
         float mx0 = -INFINITY, mx1 = -INFINITY;

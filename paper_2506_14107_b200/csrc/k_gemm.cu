@@ -254,10 +254,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         rrow_s[lane] = e.resid ? (e.resid_rows ? __ldg(e.resid_rows + mm) : mm) : 0;
       }
       const int nvalid = min(32, M - row0);     // rows of this warp that exist (may be <= 0)
+      __syncwarp();
+      const int c_beg = half * (BN / 64), c_end = (half + 1) * (BN / 64);
+      // Residual rows are known before the accumulator is: load chunk c+1's residual while
+      // chunk c is processed (8 x 16 B in flight per lane; the first batch overlaps the MMA).
+      float4 xn[8];
+      auto load_resid = [&](int c, float4 (&x)[8]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 4 + rsub;
+          x[i] = rr < nvalid ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld +
+                                                                nb * BN + c * 32 + c4)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      if (e.resid) load_resid(c_beg, xn);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = c_beg; c < c_end; ++c) {
+        float4 xc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+        if (e.resid && c + 1 < c_end) load_resid(c + 1, xn);
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
 #pragma unroll
@@ -273,52 +292,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
         if (e.bias) b = __ldg(reinterpret_cast<const float4*>(e.bias + n0));
 #pragma unroll
-        for (int ih = 0; ih < 2; ++ih) {      // two passes of 4 rows: 4 residual loads in flight
-          float4 v[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int rr = (ih * 4 + k) * 4 + rsub;
-            const float4 t4 = lds128(tile_u + rr * 128 + (((lane & 7) ^ (rr & 7)) << 4));
-            v[k].x = t4.x + b.x;
-            v[k].y = t4.y + b.y;
-            v[k].z = t4.z + b.z;
-            v[k].w = t4.w + b.w;
-          }
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 4 + rsub;
+          const float4 t4 = lds128(tile_u + rr * 128 + (((lane & 7) ^ (rr & 7)) << 4));
+          float4 v = make_float4(t4.x + b.x, t4.y + b.y, t4.z + b.z, t4.w + b.w);
           if (e.act == 1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              v[k].x = quick_gelu_fast(v[k].x); v[k].y = quick_gelu_fast(v[k].y);
-              v[k].z = quick_gelu_fast(v[k].z); v[k].w = quick_gelu_fast(v[k].w);
-            }
+            v.x = quick_gelu_fast(v.x); v.y = quick_gelu_fast(v.y);
+            v.z = quick_gelu_fast(v.z); v.w = quick_gelu_fast(v.w);
           }
-          if (e.resid) {
-            float4 x[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int i = ih * 4 + k;
-              const int rr = i * 4 + rsub;
-              x[k] = rr < nvalid ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld + n0)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) { v[k].x += x[k].x; v[k].y += x[k].y; v[k].z += x[k].z; v[k].w += x[k].w; }
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int i = ih * 4 + k;
-            const int rr = i * 4 + rsub;
-            if (rr >= nvalid) continue;
-            const int m = row0 + rr;
-            const int orr = second ? (e.out2_rows ? __ldg(e.out2_rows + m) : m) : orow_s[rr];
-            const long long off = (long long)orr * ld + col;
-            if (obf16) {
-              uint2 u;
-              u.x = pack_bf16x2(v[k].x, v[k].y);
-              u.y = pack_bf16x2(v[k].z, v[k].w);
-              *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(base) + off) = u;
-            } else {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = v[k];
-            }
+          if (e.resid) { v.x += xc[i].x; v.y += xc[i].y; v.z += xc[i].z; v.w += xc[i].w; }
+          if (rr >= nvalid) continue;
+          const int m = row0 + rr;
+          const int orr = second ? (e.out2_rows ? __ldg(e.out2_rows + m) : m) : orow_s[rr];
+          const long long off = (long long)orr * ld + col;
+          if (obf16) {
+            uint2 u;
+            u.x = pack_bf16x2(v.x, v.y);
+            u.y = pack_bf16x2(v.z, v.w);
+            *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(base) + off) = u;
+          } else {
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = v;
           }
         }
         __syncwarp();
