@@ -346,7 +346,7 @@ def main():
     peaks = measured_peaks()
     step_ms_prof = sum(p["ms"] for p in prof)
     dom = max(prof, key=lambda p: p["ms"])
-    is_tc = dom["flops"] > 0 and dom["name"].startswith("gemm")
+    is_tc = dom["flops"] > 0          # GEMMs and attention are tensor-core work
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
