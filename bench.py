@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--attn-tc", action="store_true", help="tcgen05 attention kernel (RV_ATTN_TC)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -259,7 +260,7 @@ def main():
         p_msk = torch.zeros((n_max, L * N), dtype=torch.uint8, device=dev)
 
     def step(profile):
-        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile)
+        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=args.attn_tc)
         st = m.wait()
         if world > 1:     # NCCL over NVLink only to gather embeddings + masks
             p_emb[:n_loc].copy_(emb)

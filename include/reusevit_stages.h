@@ -56,10 +56,12 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
  * KV [slots][T][2D] bf16 (K in columns 0..D-1, V in D..2D-1, head h = columns h*dh..),
  * out [M_C][D] bf16 = softmax(q K^T / sqrt(dh)) V per head; pcls [slots][H][N] fp32 (or
  * NULL) = per-head CLS softmax row over the patch keys; its head mean is t for the next
- * layer. */
+ * layer.  q_rows = allocated rows of q (>= qoff[n_w]; the tcgen05 path
+ * reads q with TMA in 128-row tiles).  use_tc selects the tcgen05/TMEM kernel (d_h = 64,
+ * 128 <= T <= 320; RV_ECONTRACT otherwise), else the mma.sync kernel (any supported shape). */
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
-                             const int32_t* qoff, const void* q, const void* KV, void* out,
-                             float* pcls, void* stream);
+                             const int32_t* qoff, const void* q, int32_t q_rows, const void* KV,
+                             void* out, float* pcls, int32_t use_tc, void* stream);
 
 #ifdef __cplusplus
 }

@@ -391,6 +391,11 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
 
 }  // namespace
 
+bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, int box_rows, char* err,
+                    size_t errlen) {
+  return encode_2d(m, ptr, rows, cols, box_rows, err, errlen);
+}
+
 bool gemm_make_plan(GemmPlan* p, const void* A, long long a_rows, const void* B, int N, int K, char* err,
                     size_t errlen) {
   if (K % BK != 0 || N % 64 != 0) {

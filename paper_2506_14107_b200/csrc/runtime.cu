@@ -81,6 +81,7 @@ struct rv_ctx {
   unsigned long long* reuse_ctr = nullptr;   // [L]
   // GEMM plans (tensor maps) bound to the buffers above
   GemmPlan pe;
+  CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 128} (tcgen05 attention)
   std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
   // ---- graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -295,6 +296,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   ctx->capR = capR;
   ctx->wdesc_cap = max_w;
   char e[256];
+  if (!make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 128, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
   if (!gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e))
     return fail(ctx, RV_ECUDA, "%s", e);
   const int L = ctx->L;
@@ -413,9 +415,15 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       if (wv.any_ref) { r.begin(K_RGATHER,l,wi); r.chk(launch_rgather(Xin, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather"); }
       // a8: attention over all T keys; CLS row -> t for layer l+1
       r.begin(K_ATTN,l,wi);
-      r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff,
-                             (!dense && l + 1 < L) ? ctx->pclsh : nullptr, n_w, T, D, H, s),
-            "attention");
+      {
+        float* pcl = (!dense && l + 1 < L) ? ctx->pclsh : nullptr;
+        if ((flags & RV_ATTN_TC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM kernel (opt-in)
+          r.chk(launch_attention_tc(ctx->tmQ, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
+                "attention");
+        else
+          r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
+                "attention");
+      }
       // a9: W_o + residual (gathered X_{l-1} rows)
       {
         Epi e;
@@ -974,11 +982,23 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
 }
 
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const int32_t* qoff, const void* q,
-                             const void* KV, void* out, float* pcls, void* stream) {
+                             int32_t q_rows, const void* KV, void* out, float* pcls, int32_t use_tc,
+                             void* stream) {
   if (!ctx) return RV_ECONTRACT;
+  if (q_rows < 1 || !q || !KV || !out) return fail(ctx, RV_ECONTRACT, "rv_stage_attention: bad arguments");
   CK(cudaSetDevice(ctx->device));
-  CK(launch_attention((const bf16*)q, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D,
-                      ctx->H, (cudaStream_t)stream));
+  if (use_tc && !attn_tc_supported(ctx->T, ctx->D, ctx->H))
+    return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and 128 <= T <= 320");
+  if (use_tc) {
+    CUtensorMap tm;
+    char e[256];
+    if (!make_tmap_bf16(&tm, q, q_rows, ctx->D, 128, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+    CK(launch_attention_tc(tm, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
+                           (cudaStream_t)stream));
+  } else {
+    CK(launch_attention((const bf16*)q, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T,
+                        ctx->D, ctx->H, (cudaStream_t)stream));
+  }
   return RV_OK;
 }
 

@@ -66,7 +66,15 @@ cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmas
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
                            unsigned long long* reuse_ctr, int* count_log, cudaStream_t s);
 
-// ---------------------------------------------------------------- attention (k_attn.cu)
+// 2D bf16 tensor map, box {64 cols, box_rows}, SWIZZLE_128B (k_gemm.cu)
+bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, int box_rows, char* err,
+                    size_t errlen);
+
+// ---------------------------------------------------------------- attention (k_attn_tc.cu, k_attn.cu)
+bool attn_tc_supported(int T, int D, int H);
+cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const bf16* KV, const int* kvsrc, bf16* out,
+                                const int* wdesc, const int* qoff, float* pclsh, int n_w, int T, int D, int H,
+                                cudaStream_t s);
 cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
                              const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s);
 }  // namespace rv

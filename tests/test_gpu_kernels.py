@@ -71,8 +71,9 @@ def test_gemm_row_position_invariance(dev):
 
 
 # ------------------------------------------------------------------------- attention
-@pytest.mark.parametrize("cfgname", ["tiny", "b16", "l14"])
-def test_attention_vs_torch(dev, cfgname):
+@pytest.mark.parametrize("cfgname,use_tc", [("tiny", False), ("b16", False), ("l14", False), ("b16", True),
+                                            ("l14", True)])
+def test_attention_vs_torch(dev, cfgname, use_tc):
     cfg = synth.CONFIGS[cfgname]
     m, _, _ = _model(cfg, gates=False)
     T, D, H, dh = cfg.T, cfg.dim, cfg.heads, cfg.dh
@@ -90,7 +91,7 @@ def test_attention_vs_torch(dev, cfgname):
     pcls = torch.zeros((slots, H, cfg.N), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
     m.stage_attention(torch.from_numpy(wdesc).to(dev), torch.from_numpy(qoff).to(dev), q.to(dev), KV.to(dev),
-                      out, pcls, st)
+                      out, pcls, st, use_tc=use_tc)
     torch.cuda.synchronize()
     for w in range(n_w):
         s = slot_of[w]

@@ -41,22 +41,26 @@ def build(cfg, **gk):
 
 
 CASES = [
-    # cfg, frames on GPU, frames checked by the oracle (prefix-closed), motion p, mode
+    # cfg, frames on GPU, frames checked by the oracle (prefix-closed), motion p, mode[, attn_tc]
     ("tiny", 8, 8, 0.3, "bimodal"),
     ("tiny", 41, 41, 0.2, "bimodal"),
     ("b16", 32, 32, 0.3, "bimodal"),
     ("b16", 32, 32, 0.1, "bimodal"),
     ("l14", 64, 21, 0.2, "bimodal"),
+    ("b16", 32, 32, 0.3, "bimodal", True),
+    ("l14", 64, 21, 0.2, "bimodal", True),
 ]
 
 
-@pytest.mark.parametrize("cfgname,n,n_check,p,mode", CASES)
-def test_embed_parity(cuda_ok, cfgname, n, n_check, p, mode):
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-n{c[1]}-p{c[3]}" + ("-tc" if len(c) > 5 else "") for c in CASES])
+def test_embed_parity(cuda_ok, case):
+    cfgname, n, n_check, p, mode = case[:5]
+    attn_tc = len(case) > 5 and case[5]
     cfg = synth.CONFIGS[cfgname]
     m, W, G = build(cfg)
     x, c = synth.make_video(cfg, n, p, seed=2000 + n)
     plan = oracle.plan_gop(n)
-    Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), want_scores=True)
+    Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), want_scores=True, attn_tc=attn_tc)
     torch.cuda.synchronize()
     frames = list(range(n_check))
     ref = oracle.reuse_embed(cfg, W, G, x, c, plan, frames=frames)
