@@ -128,6 +128,19 @@ __global__ void rgather_kernel(const float* __restrict__ X, const int* __restric
   }
 }
 
+__global__ void gather_rows_bf16_kernel(const bf16* __restrict__ src, const int* __restrict__ rows,
+                                        const int* __restrict__ count, bf16* __restrict__ dst, int D) {
+  const int M = *count;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int D8 = D >> 3;
+  for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
+    const uint4* a = reinterpret_cast<const uint4*>(src + (long long)__ldg(rows + m) * D);
+    uint4* o = reinterpret_cast<uint4*>(dst + (long long)m * D);
+#pragma unroll 4
+    for (int k = lane; k < D8; k += 32) o[k] = __ldg(a + k);
+  }
+}
+
 template <int VPL>
 __global__ void ln_post_kernel(const float* __restrict__ X, const float* __restrict__ g,
                                const float* __restrict__ b, float* __restrict__ emb, int n, int T,
@@ -185,6 +198,12 @@ cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count
 cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
                            bf16* Ar, int D, cudaStream_t s) {
   rgather_kernel<<<grid_rows(max_rows), 256, 0, s>>>(X, idxR, provrow, count, Ar, D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows_bf16(const bf16* src, const int* rows, const int* count, int max_rows, bf16* dst,
+                                   int D, cudaStream_t s) {
+  gather_rows_bf16_kernel<<<grid_rows(max_rows), 256, 0, s>>>(src, rows, count, dst, D);
   return cudaGetLastError();
 }
 

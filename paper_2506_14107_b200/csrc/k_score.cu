@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(SCORE_THREADS)
                  const int4* __restrict__ wdesc, const float* __restrict__ tsrc, int tH,
                  const float* __restrict__ codec, const uint8_t* force,
                  const float* __restrict__ gate, int Hg, int dense, uint8_t* masks, float* scores,
-                 uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntR) {
+                 uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntR,
+                 bf16* __restrict__ dfull) {
   __shared__ int s_reused;
   const int w = blockIdx.x;
   const int i_beg = 1 + blockIdx.y * SCORE_TOK;
@@ -118,6 +119,20 @@ __global__ void __launch_bounds__(SCORE_THREADS)
       wprov[(long long)w * T + i] = (uint8_t)prov;
       my_reused += M;
     }
+    if (M && dfull) {
+      // Eq. 8: Delta R_i = R_cur_i - R_ref_i, written now while both rows are cache-hot
+      // (token-indexed; the compaction gathers it into the restoration operand)
+      const float4* rr = prov ? rf : rp;
+      uint2* o = reinterpret_cast<uint2*>(dfull + ((long long)slot * T + i) * D);
+#pragma unroll 4
+      for (int k = lane; k < D4; k += 32) {
+        const float4 a = __ldg(cur + k), b = __ldg(rr + k);
+        uint2 u;
+        u.x = pack_bf16x2(a.x - b.x, a.y - b.y);
+        u.y = pack_bf16x2(a.z - b.z, a.w - b.w);
+        o[k] = u;
+      }
+    }
   }
   if (lane == 0 && my_reused) atomicAdd(&s_reused, my_reused);
   __syncthreads();
@@ -203,13 +218,13 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
 cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
-                         int* cntR, cudaStream_t s) {
+                         int* cntR, bf16* dfull, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(cntR, 0, (size_t)n_w * sizeof(int), s);
   if (e != cudaSuccess) return e;
   dim3 grid(n_w, (N + SCORE_TOK - 1) / SCORE_TOK);
   score_kernel<<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, reinterpret_cast<const int4*>(wdesc), tsrc, tH,
-                                              codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntR);
+                                              codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntR, dfull);
   return cudaGetLastError();
 }
 

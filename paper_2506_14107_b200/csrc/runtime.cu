@@ -69,6 +69,7 @@ struct rv_ctx {
   bf16* KV = nullptr;
   float* pclsh = nullptr;     // [n][H][N] per-head CLS attention of the previous layer (t)
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
+  bf16* dfull = nullptr;      // [n][T][D] Delta of reused tokens (token-indexed, bf16)
   bf16* patches_bf16 = nullptr;
   float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
   uint8_t* out_masks = nullptr;
@@ -267,6 +268,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->KV, n * T * 2 * D);
   AL(ctx->pclsh, n * ctx->H * N);
   AL(ctx->kvsrc, n * T);
+  AL(ctx->dfull, (size_t)n * T * D);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
   AL(ctx->in_patches, (size_t)n * N * ctx->pp);
   AL(ctx->in_codec, n * N);
@@ -383,7 +385,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       r.begin(K_SCORE,l,wi);
       r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
                          ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
-                         ctx->wprov, ctx->cntR, s),
+                         ctx->wprov, ctx->cntR, ctx->dfull, s),
             "score");
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
@@ -411,8 +413,12 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         r.begin(K_QKV,l,wi);
         r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
       }
-      // a7 + Eq. 8: reused rows take the provider's K/V; Delta for the restoration layer
-      if (wv.any_ref) { r.begin(K_RGATHER,l,wi); r.chk(launch_rgather(Xin, ctx->idxR, ctx->provrow, MR, maxR, ctx->Ar, D, s), "rgather"); }
+      // Eq. 8: Delta of the reused rows (written token-indexed by the score pass) -> compact
+      // restoration operand.  (a7: reused K/V are read in place through kvsrc.)
+      if (wv.any_ref) {
+        r.begin(K_RGATHER, l, wi);
+        r.chk(launch_gather_rows_bf16(ctx->dfull, ctx->idxR, MR, maxR, ctx->Ar, D, s), "rgather");
+      }
       // a8: attention over all T keys; CLS row -> t for layer l+1
       r.begin(K_ATTN,l,wi);
       {
@@ -917,11 +923,11 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
       case K_PATCH: a.bytes += n * N * (ctx->pp * 4.0 + ctx->KP * 2.0); break;
       case K_PE: a.flops += 2.0 * n * N * ctx->pp * D; a.bytes += n * N * (ctx->KP * 2.0 + D * 4.0); break;
       case K_EMBED: a.bytes += n * T * D * 8.0; break;
-      case K_SCORE: a.bytes += (wdec[r.w] + wrefs[r.w]) * N * D * 4.0 + wdec[r.w] * N * 10.0; break;
+      case K_SCORE: a.bytes += (wdec[r.w] + wrefs[r.w]) * N * D * 4.0 + wdec[r.w] * N * 10.0 + MR * D * 2.0; break;
       case K_COMPACT: a.bytes += nw * T * 2.0 + (MC + 2 * MR) * 4.0; break;
       case K_GATHER: a.bytes += MC * (D * 4.0 + D * 2.0 + 4.0); break;
       case K_QKV: a.flops += 2.0 * MC * 3 * D * D; a.bytes += MC * (D * 2.0 + 3 * D * 2.0) + 3 * D * D * 2.0; break;
-      case K_RGATHER: a.bytes += MR * (2 * D * 4.0 + D * 2.0 + 2 * (2 * D * 2.0) + 8.0); break;
+      case K_RGATHER: a.bytes += MR * (D * 2.0 + D * 2.0 + 4.0); break;
       case K_ATTN: a.flops += 4.0 * MC * T * D; a.bytes += MC * D * 4.0 + nw * T * 2 * D * 2.0; break;
       case K_CLS: a.bytes += nw * (T * D * 2.0 + D * 2.0 + N * 4.0); break;
       case K_WO: a.flops += 2.0 * MC * D * D; a.bytes += MC * (D * 2.0 + D * 4.0 + D * 4.0) + D * D * 2.0; break;
@@ -948,7 +954,7 @@ rv_status rv_stage_score(rv_ctx* ctx, int32_t layer, const float* X, int32_t n_w
   if (layer < 0 || layer >= ctx->L || n_w < 0) return fail(ctx, RV_ECONTRACT, "rv_stage_score: bad layer/n_w");
   CK(cudaSetDevice(ctx->device));
   CK(launch_score(X, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, 1, codec, force, ctx->lw[layer].gate,
-                  ctx->Hg, 0, masks, scores, wmask, wprov, cntR, (cudaStream_t)stream));
+                  ctx->Hg, 0, masks, scores, wmask, wprov, cntR, nullptr, (cudaStream_t)stream));
   return RV_OK;
 }
 

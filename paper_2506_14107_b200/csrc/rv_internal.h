@@ -54,6 +54,9 @@ cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count
                              const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
 cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
                            bf16* Ar, int D, cudaStream_t s);
+// Ar[m] = dfull[idxR[m]] (bf16 rows of D): the restoration operand from the score pass's Delta
+cudaError_t launch_gather_rows_bf16(const bf16* src, const int* rows, const int* count, int max_rows, bf16* dst,
+                                   int D, cudaStream_t s);
 cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
                            cudaStream_t s);
 
@@ -61,7 +64,7 @@ cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float
 cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
-                         int* cntR, cudaStream_t s);
+                         int* cntR, bf16* dfull, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
                            unsigned long long* reuse_ctr, int* count_log, cudaStream_t s);
