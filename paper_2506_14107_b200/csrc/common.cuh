@@ -30,6 +30,13 @@ RV_DEV int warp_sum_i(int v) {
 // __expf: the decision logit's sign is compared with the oracle's.
 RV_DEV float quick_gelu(float x) { return x / (1.0f + expf(-1.702f * x)); }
 
+// 2^x on the MUFU (ex2.approx.ftz): softmax terms, arguments <= 0.
+RV_DEV float ex2f_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 RV_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // RNE (cvt.rn.bf16x2.f32)
   return *reinterpret_cast<uint32_t*>(&h);

@@ -40,6 +40,9 @@ template <int DH>
 RV_DEV void load_kv_block(bf16* Kb, bf16* Vb, const bf16* __restrict__ KV, const int* rows_s, int k0, int Tp, int T,
                           long long ld, int D, int h, int tid) {
   constexpr int KS = DH + 8, CH = DH / 8;
+#ifdef RV_ATTN_NO_LOAD   // microbenchmark hook (tools/attn_bench.cu): compute without K/V traffic
+  return;
+#endif
   const int nrow = min(KB, Tp - k0);
   for (int idx = tid; idx < nrow * CH; idx += 128) {
     const int j = idx / CH, c = idx % CH;
@@ -120,7 +123,11 @@ __global__ void __launch_bounds__(128)
           qa[kk][3] = *reinterpret_cast<const uint32_t*>(Qs + (r0 + g + 8) * KS + kk * 16 + 8 + 2 * tq);
         }
       }
+#ifdef RV_ATTN_NO_MMA      // microbenchmark hook (tools/attn_bench.cu): K/V traffic only
+      if (false) {
+#else
       if (active) {
+#endif
         const bf16* Ks = Kr + buf * KB * KS;
         const bf16* Vs = Vr + buf * KB * KS;
         const int k0 = kb * KB;
@@ -145,14 +152,19 @@ __global__ void __launch_bounds__(128)
             }
           }
         }
+        if (k0 + KB > T) {      // last block: mask padded keys
 #pragma unroll
-        for (int j = 0; j < KB / 8; ++j) {
-          const int col = k0 + j * 8 + 2 * tq;
-          if (j >= nj || col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
-          if (j >= nj || col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
-          if (qt == 0 && warp == 0 && g == 0 && j < nj) {   // raw logits of the CLS row (row 0)
-            scls[col] = s[j][0];
-            scls[col + 1] = s[j][1];
+          for (int j = 0; j < KB / 8; ++j) {
+            const int col = k0 + j * 8 + 2 * tq;
+            if (j >= nj || col >= T) { s[j][0] = -INFINITY; s[j][2] = -INFINITY; }
+            if (j >= nj || col + 1 >= T) { s[j][1] = -INFINITY; s[j][3] = -INFINITY; }
+          }
+        }
+        if (qt == 0 && warp == 0 && g == 0) {   // raw logits of the CLS row (row 0)
+#pragma unroll
+          for (int j = 0; j < KB / 8; ++j) {
+            const int col = k0 + j * 8 + 2 * tq;
+            if (j < nj) { scls[col] = s[j][0]; scls[col + 1] = s[j][1]; }
           }
         }
         float mx0 = -INFINITY, mx1 = -INFINITY;
@@ -166,15 +178,15 @@ __global__ void __launch_bounds__(128)
         mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
         mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
         const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-        const float a0 = exp2f((m0 - mn0) * scale_log2), a1 = exp2f((m1 - mn1) * scale_log2);
+        const float a0 = ex2f_fast((m0 - mn0) * scale_log2), a1 = ex2f_fast((m1 - mn1) * scale_log2);
         const float ms0 = mn0 * scale_log2, ms1 = mn1 * scale_log2;
         float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
         for (int j = 0; j < KB / 8; ++j) {
-          s[j][0] = exp2f(fmaf(s[j][0], scale_log2, -ms0));
-          s[j][1] = exp2f(fmaf(s[j][1], scale_log2, -ms0));
-          s[j][2] = exp2f(fmaf(s[j][2], scale_log2, -ms1));
-          s[j][3] = exp2f(fmaf(s[j][3], scale_log2, -ms1));
+          s[j][0] = ex2f_fast(fmaf(s[j][0], scale_log2, -ms0));
+          s[j][1] = ex2f_fast(fmaf(s[j][1], scale_log2, -ms0));
+          s[j][2] = ex2f_fast(fmaf(s[j][2], scale_log2, -ms1));
+          s[j][3] = ex2f_fast(fmaf(s[j][3], scale_log2, -ms1));
           rs0 += s[j][0] + s[j][1];
           rs1 += s[j][2] + s[j][3];
         }
@@ -233,7 +245,7 @@ __global__ void __launch_bounds__(128)
       __syncthreads();
       const float mcls = s_cls[0], linv = 1.f / s_cls[1];
       for (int j = 1 + tid; j < T; j += 128)
-        pclsh[((long long)slot * H + h) * (T - 1) + (j - 1)] = exp2f((scls[j] - mcls) * scale_log2) * linv;
+        pclsh[((long long)slot * H + h) * (T - 1) + (j - 1)] = ex2f_fast((scls[j] - mcls) * scale_log2) * linv;
     }
   }
 }

@@ -397,14 +397,14 @@ bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, i
 }
 
 bool gemm_make_plan(GemmPlan* p, const void* A, long long a_rows, const void* B, int N, int K, char* err,
-                    size_t errlen) {
+                    size_t errlen, int bn_max) {
   if (K % BK != 0 || N % 64 != 0) {
     snprintf(err, errlen, "gemm: K=%d must be a multiple of 64 and N=%d a multiple of 64", K, N);
     return false;
   }
   p->N = N;
   p->K = K;
-  p->BN = (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : 64);
+  p->BN = (N % 256 == 0 && bn_max >= 256) ? 256 : ((N % 128 == 0 && bn_max >= 128) ? 128 : 64);
   return encode_2d(&p->tmA, A, a_rows, K, BM, err, errlen) && encode_2d(&p->tmB, B, N, K, p->BN, err, errlen);
 }
 

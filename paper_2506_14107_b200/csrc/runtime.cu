@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -302,17 +303,21 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   if (!gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e))
     return fail(ctx, RV_ECUDA, "%s", e);
   const int L = ctx->L;
+  // N-tile of the residual-streaming GEMMs (W_o, FC2, restoration R2); RV_BN_RESID / RV_BN_R2
+  // override for experiments.
+  const int bn_resid = getenv("RV_BN_RESID") ? atoi(getenv("RV_BN_RESID")) : 256;
+  const int bn_r2 = getenv("RV_BN_R2") ? atoi(getenv("RV_BN_R2")) : 256;
   ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
   ctx->g_r1.resize(L); ctx->g_r2.resize(L);
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
     bool ok = gemm_make_plan(&ctx->g_qkv[l], ctx->A, capC, w.Wqkv, 3 * (int)D, (int)D, e, sizeof e) &&
-              gemm_make_plan(&ctx->g_wo[l], ctx->att, capC, w.Wo, (int)D, (int)D, e, sizeof e) &&
+              gemm_make_plan(&ctx->g_wo[l], ctx->att, capC, w.Wo, (int)D, (int)D, e, sizeof e, bn_resid) &&
               gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
-              gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e);
+              gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e, bn_resid);
     if (ok && ctx->gates_loaded)
       ok = gemm_make_plan(&ctx->g_r1[l], ctx->Ar, capR, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
-           gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e);
+           gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
     if (!ok) return fail(ctx, RV_ECUDA, "%s", e);
   }
   return RV_OK;

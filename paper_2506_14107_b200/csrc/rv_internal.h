@@ -38,8 +38,10 @@ struct GemmPlan {
 };
 
 // Encode the tensor maps for a GEMM with A = [a_rows][K] and B = [N][K] (bf16, row-major).
+// bn_max caps the N tile (256 / 128 / 64): residual-streaming epilogues prefer 128 (all of a
+// tile's residual rows in flight before its accumulator is ready).
 bool gemm_make_plan(GemmPlan* p, const void* A, long long a_rows, const void* B, int N, int K,
-                    char* err, size_t errlen);
+                    char* err, size_t errlen, int bn_max = 256);
 // Launch: M read from *M_dev when M_dev != nullptr, else M_host.  max_m = host upper bound of
 // M (sizes the persistent grid).
 cudaError_t gemm_launch(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
