@@ -32,15 +32,21 @@ constexpr int BK = 64;            // 64 bf16 = 128 B = one SWIZZLE_128B atom row
 constexpr int GEMM_THREADS = 320;   // TMA warp + MMA/TMEM warp + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 
-template <int BN>
+constexpr int RDEPTH = 3;         // residual chunks in flight per epilogue warp (SR variant)
+
+// SR ("short K, streaming residual"): for K <= 256 the mainloop needs only 2 stages, and the
+// freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep, so the
+// HBM-bound epilogue keeps ~96 KB of residual loads in flight per SM.
+template <int BN, bool SR>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = SR ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int STAGE_OUT = EPI_WARPS * (32 * 32 + 64) * 4;   // per-warp 32x32 fp32 transpose tile + row maps
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT + 256 /*barriers*/;
+  static constexpr int RESID = SR ? EPI_WARPS * RDEPTH * 32 * 32 * 4 : 0;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT + RESID + 256 /*barriers*/;
   static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
@@ -140,17 +146,18 @@ RV_DEV float quick_gelu_fast(float x) {
   return x * fmaf(0.5f, t, 0.5f);
 }
 
-template <int BN>
+template <int BN, bool SR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, SR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // SWIZZLE_128B needs 1024-B aligned stages
   uint8_t* smem = smem_raw;
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   float* sOut = reinterpret_cast<float*>(sB + C::STAGES * C::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sOut) + C::STAGE_OUT);
+  float* sRes = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sOut) + C::STAGE_OUT);   // SR ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sOut) + C::STAGE_OUT + C::RESID);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -268,15 +275,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                              : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       };
-      if (e.resid) load_resid(c_beg, xn);
+      // SR: this lane's 8 x 16 B of chunk c go to ring slot c % RDEPTH (read back by the same
+      // lane, so a per-thread cp.async.wait_group is the only synchronisation needed)
+      const uint32_t ring = smem_u32(sRes + (warp - 2) * RDEPTH * 1024);
+      auto issue_resid = [&](int c) {
+        if (c < c_end) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + rsub;
+            const float* src = e.resid + (long long)rrow_s[rr < nvalid ? rr : 0] * e.resid_ld + nb * BN + c * 32 + c4;
+            const uint32_t dst = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                         "r"(rr < nvalid ? 16 : 0)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");   // one group per chunk slot (maybe empty)
+      };
+      if (e.resid) {
+        if constexpr (SR) {
+          for (int k = 0; k < RDEPTH; ++k) issue_resid(c_beg + k);
+        } else {
+          load_resid(c_beg, xn);
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
       for (int c = c_beg; c < c_end; ++c) {
         float4 xc[8];
+        if constexpr (SR) {
+          if (e.resid) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(RDEPTH - 1) : "memory");
 #pragma unroll
-        for (int i = 0; i < 8; ++i) xc[i] = xn[i];
-        if (e.resid && c + 1 < c_end) load_resid(c + 1, xn);
+            for (int i = 0; i < 8; ++i) {
+              const int rr = i * 4 + rsub;
+              xc[i] = lds128(ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xc[i] = xn[i];
+          if (e.resid && c + 1 < c_end) load_resid(c + 1, xn);
+        }
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
 #pragma unroll
@@ -313,6 +354,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           } else {
             *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = v;
           }
+        }
+        if constexpr (SR) {
+          if (e.resid) issue_resid(c + RDEPTH);   // refill the slot consumed above
         }
         __syncwarp();
       }
@@ -375,17 +419,34 @@ int num_sms() {
 template <int BN>
 cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
                       cudaStream_t s) {
-  using C = Cfg<BN>;
+  // short K with a residual: 2-stage mainloop + cp.async residual ring (see Cfg)
+  if (p.K <= 2 * BK && e.resid) {
+    using C = Cfg<BN, true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t err =
+          cudaFuncSetAttribute(gemm_tc_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      if (err != cudaSuccess) return err;
+      attr = true;
+    }
+    const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    if (grid < 1) grid = 1;
+    gemm_tc_kernel<BN, true><<<grid, GEMM_THREADS, C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+    return cudaGetLastError();
+  }
+  using C = Cfg<BN, false>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t err =
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (err != cudaSuccess) return err;
     attr = true;
   }
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+  gemm_tc_kernel<BN, false><<<grid, GEMM_THREADS, C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
   return cudaGetLastError();
 }
 
