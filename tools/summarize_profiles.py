@@ -42,7 +42,7 @@ def classify(names):
         elif "gather_ln" in n:
             out.append("gather_ln1" if ln == 0 else "ln2")
             ln += 1
-        elif "rgather" in n:
+        elif "rgather" in n or "gather_rows" in n:
             out.append("rgather")
         elif "attn_kernel" in n:
             out.append("attention")
