@@ -58,7 +58,7 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
  * NULL) = per-head CLS softmax row over the patch keys; its head mean is t for the next
  * layer.  q_rows = allocated rows of q (>= qoff[n_w]; the tcgen05 path
  * reads q with TMA in 128-row tiles).  use_tc selects the tcgen05/TMEM kernel (d_h = 64,
- * 128 <= T <= 320; RV_ECONTRACT otherwise), else the mma.sync kernel (any supported shape). */
+ * T - 1 <= 256; RV_ECONTRACT otherwise), else the mma.sync kernel (any supported shape). */
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
                              const int32_t* qoff, const void* q, int32_t q_rows, const void* KV,
                              void* out, float* pcls, int32_t use_tc, void* stream);

@@ -59,5 +59,18 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+def build_variant(out_path: str, defines=()) -> str:
+    """Experiment builds (e.g. -DRV_ATTN_TRACE): all sources with extra -D flags into out_path;
+    load with _lib.load_library(out_path) before the first ReuseViT.  Never the product library."""
+    os.makedirs(os.path.dirname(out_path), exist_ok=True)
+    objs = []
+    for src in sources():
+        obj = out_path + "." + os.path.basename(src) + ".o"
+        subprocess.run([NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj], check=True)
+        objs.append(obj)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", out_path, *objs, "-cudart", "static"], check=True)
+    return out_path
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,10 +1,8 @@
-// k_elem.cu — HBM-bound row kernels of the hot path (SURVEY §8(a) a1, a5, a7, a12, a14).
+// k_elem.cu — HBM-bound row kernels of the hot path (SURVEY §8(a) a1, a5, a14).
 //
 //   patch_to_bf16 : fp32 patches [rows][pp] -> bf16 GEMM operand [rows][KP] (zero K padding)
 //   embed_finish  : X0 = LN_pre(concat(cls, patches W_pe) + pos) in place, t := 1/N
 //   gather_ln     : A[m] = bf16(LN(src[rows[m]]))  — gather of recompute rows + LN1/LN2 (a5)
-//   rgather       : reused rows: Delta = X[row] - X[provrow] -> bf16 (Eq. 8) and the
-//                   reuse-cache read K_l,V_l[row] <- K_l,V_l[provrow] (a7)
 //   ln_post       : Z_f = LN_post(X_L[f][CLS])
 // One warp per row; lane j owns elements j, j+32, ... (coalesced 128 B per warp access);
 // LN statistics in fp32 with a fixed butterfly reduction order (deterministic).
@@ -106,41 +104,6 @@ __global__ void gather_ln_kernel(const float* __restrict__ src, const int* __res
   }
 }
 
-// Delta R = X_{l-1}[row] - X_{l-1}[provrow] -> bf16 operand of the restoration layer (Eq. 8).
-__global__ void rgather_kernel(const float* __restrict__ X, const int* __restrict__ idxR,
-                               const int* __restrict__ provrow, const int* __restrict__ count,
-                               bf16* __restrict__ Ar, int D) {
-  const int M = *count;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int D4 = D >> 2;
-  for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
-    const float4* xr = reinterpret_cast<const float4*>(X + (long long)__ldg(idxR + m) * D);
-    const float4* xp = reinterpret_cast<const float4*>(X + (long long)__ldg(provrow + m) * D);
-    uint2* o = reinterpret_cast<uint2*>(Ar + (long long)m * D);
-#pragma unroll 4
-    for (int k = lane; k < D4; k += 32) {
-      const float4 a = __ldg(xr + k), b = __ldg(xp + k);
-      uint2 u;
-      u.x = pack_bf16x2(a.x - b.x, a.y - b.y);
-      u.y = pack_bf16x2(a.z - b.z, a.w - b.w);
-      o[k] = u;
-    }
-  }
-}
-
-__global__ void gather_rows_bf16_kernel(const bf16* __restrict__ src, const int* __restrict__ rows,
-                                        const int* __restrict__ count, bf16* __restrict__ dst, int D) {
-  const int M = *count;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int D8 = D >> 3;
-  for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
-    const uint4* a = reinterpret_cast<const uint4*>(src + (long long)__ldg(rows + m) * D);
-    uint4* o = reinterpret_cast<uint4*>(dst + (long long)m * D);
-#pragma unroll 4
-    for (int k = lane; k < D8; k += 32) o[k] = __ldg(a + k);
-  }
-}
-
 template <int VPL>
 __global__ void ln_post_kernel(const float* __restrict__ X, const float* __restrict__ g,
                                const float* __restrict__ b, float* __restrict__ emb, int n, int T,
@@ -192,18 +155,6 @@ cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count
   if (v <= 2) gather_ln_kernel<2><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
   else if (v <= 24) gather_ln_kernel<24><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
   else gather_ln_kernel<32><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
-                           bf16* Ar, int D, cudaStream_t s) {
-  rgather_kernel<<<grid_rows(max_rows), 256, 0, s>>>(X, idxR, provrow, count, Ar, D);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gather_rows_bf16(const bf16* src, const int* rows, const int* count, int max_rows, bf16* dst,
-                                   int D, cudaStream_t s) {
-  gather_rows_bf16_kernel<<<grid_rows(max_rows), 256, 0, s>>>(src, rows, count, dst, D);
   return cudaGetLastError();
 }
 

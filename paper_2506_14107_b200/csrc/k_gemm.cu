@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int rr = i * 4 + rsub;
-          x[i] = rr < nvalid ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld +
+          x[i] = (rr < nvalid && orow_s[rr] >= 0) ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld +
                                                                 nb * BN + c * 32 + c4)
                              : make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -283,10 +283,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int rr = i * 4 + rsub;
-            const float* src = e.resid + (long long)rrow_s[rr < nvalid ? rr : 0] * e.resid_ld + nb * BN + c * 32 + c4;
+            const bool live = rr < nvalid && orow_s[rr] >= 0;
+            const float* src = e.resid + (long long)rrow_s[live ? rr : 0] * e.resid_ld + nb * BN + c * 32 + c4;
             const uint32_t dst = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                         "r"(rr < nvalid ? 16 : 0)
+                         "r"(live ? 16 : 0)
                          : "memory");
           }
         }
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (rr >= nvalid) continue;
           const int m = row0 + rr;
           const int orr = second ? (e.out2_rows ? __ldg(e.out2_rows + m) : m) : orow_s[rr];
+          if (orr < 0) continue;   // row map -1: result not stored (restoration over C rows)
           const long long off = (long long)orr * ld + col;
           if (obf16) {
             uint2 u;

@@ -21,6 +21,10 @@ namespace {
 constexpr int SCORE_THREADS = 256;
 constexpr int SCORE_TOK = 32;      // tokens per CTA (8 warps x 4 tokens): grid = n_w x ceil(N/32)
 
+// VPL > 0: D == 128 * VPL, the token's 3 x VPL float4 per lane are loaded unconditionally
+// (a missing reference re-reads the current row, an L1 hit) and without a loop-carried branch,
+// so all of them are in flight together; VPL == 0: generic D.
+template <int VPL>
 __global__ void __launch_bounds__(SCORE_THREADS)
     score_kernel(const float* __restrict__ X, int T, int D, int N, int L, int layer,
                  const int4* __restrict__ wdesc, const float* __restrict__ tsrc, int tH,
@@ -71,6 +75,28 @@ __global__ void __launch_bounds__(SCORE_THREADS)
     const float4* rp = past >= 0 ? reinterpret_cast<const float4*>(X + ((long long)past * T + i) * D) : nullptr;
     const float4* rf = fut >= 0 ? reinterpret_cast<const float4*>(X + ((long long)fut * T + i) * D) : nullptr;
     float cc = 0.f, pp = 0.f, ff = 0.f, cp = 0.f, cf = 0.f;
+    if constexpr (VPL > 0) {
+      const float4* rp2 = rp ? rp : cur;
+      const float4* rf2 = rf ? rf : cur;
+      float4 cv[VPL], pv[VPL], fv[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        cv[j] = __ldg(cur + lane + 32 * j);
+        pv[j] = __ldg(rp2 + lane + 32 * j);
+        fv[j] = __ldg(rf2 + lane + 32 * j);
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const float4 c = cv[j], p = pv[j], f = fv[j];
+        cc += c.x * c.x + c.y * c.y + c.z * c.z + c.w * c.w;
+        pp += p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w;
+        cp += c.x * p.x + c.y * p.y + c.z * p.z + c.w * p.w;
+        ff += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+        cf += c.x * f.x + c.y * f.y + c.z * f.z + c.w * f.w;
+      }
+      if (!rp) pp = cp = 0.f;
+      if (!rf) ff = cf = 0.f;
+    } else
 #pragma unroll 4
     for (int k = lane; k < D4; k += 32) {
       const float4 c = __ldg(cur + k);
@@ -120,10 +146,10 @@ __global__ void __launch_bounds__(SCORE_THREADS)
       my_reused += M;
     }
     if (M && dfull) {
-      // Eq. 8: Delta R_i = R_cur_i - R_ref_i, written now while both rows are cache-hot
-      // (token-indexed; the compaction gathers it into the restoration operand)
+      // Eq. 8: Delta R_i = R_cur_i - R_ref_i, written now while both rows are cache-hot, to
+      // the wave-local token row w*T + i: the restoration GEMM reads it there in place
       const float4* rr = prov ? rf : rp;
-      uint2* o = reinterpret_cast<uint2*>(dfull + ((long long)slot * T + i) * D);
+      uint2* o = reinterpret_cast<uint2*>(dfull + ((long long)w * T + i) * D);
 #pragma unroll 4
       for (int k = lane; k < D4; k += 32) {
         const float4 a = __ldg(cur + k), b = __ldg(rr + k);
@@ -145,7 +171,8 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
     compact_kernel(int n_w, int T, const int4* __restrict__ wdesc, const uint8_t* __restrict__ wmask,
                    const uint8_t* __restrict__ wprov, const int* __restrict__ cntR, int* __restrict__ idxC,
                    int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
-                   int* __restrict__ counts, int* kvsrc, unsigned long long* reuse_ctr, int* count_log) {
+                   int* __restrict__ counts, int* kvsrc, unsigned long long* reuse_ctr, int* count_log,
+                   int* __restrict__ rpos) {
   __shared__ int s_part[COMPACT_THREADS / 32];
   __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
   __shared__ int s_base[2];
@@ -195,12 +222,14 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
     }
     const unsigned lt = (1u << lane) - 1u;
     if (isC) {
+      if (rpos) rpos[(long long)w * T + i] = -1;   // restoration row map: not reused
       idxC[offC + pc + __popc(bc & lt)] = slot * T + i;
       if (kvsrc) kvsrc[(long long)slot * T + i] = slot * T + i;
     }
     if (isR) {
       const int r = offR + pr + __popc(br & lt);
       const int prow = (pv[i] ? d4.z : d4.y) * T + i;
+      if (rpos) rpos[(long long)w * T + i] = r;
       idxR[r] = slot * T + i;
       provrow[r] = prow;
       // reuse-cache read in place: K/V of a reused token = its provider's (already final,
@@ -223,17 +252,24 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
   cudaError_t e = cudaMemsetAsync(cntR, 0, (size_t)n_w * sizeof(int), s);
   if (e != cudaSuccess) return e;
   dim3 grid(n_w, (N + SCORE_TOK - 1) / SCORE_TOK);
-  score_kernel<<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, reinterpret_cast<const int4*>(wdesc), tsrc, tH,
-                                              codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntR, dfull);
+  const int4* wd = reinterpret_cast<const int4*>(wdesc);
+#define RV_SCORE(V)                                                                                              \
+  score_kernel<V><<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, wd, tsrc, tH, codec, force, gate, Hg, dense, \
+                                                 masks, scores, wmask, wprov, cntR, dfull)
+  if (D == 1024) RV_SCORE(8);
+  else if (D == 768) RV_SCORE(6);
+  else RV_SCORE(0);
+#undef RV_SCORE
   return cudaGetLastError();
 }
 
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, cudaStream_t s) {
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
   compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
-                                                 cntR, idxC, idxR, provrow, qoff, counts, kvsrc, reuse_ctr, count_log);
+                                                 cntR, idxC, idxR, provrow, qoff, counts, kvsrc, reuse_ctr, count_log,
+                                                 rpos);
   return cudaGetLastError();
 }
 

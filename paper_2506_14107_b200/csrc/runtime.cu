@@ -70,7 +70,8 @@ struct rv_ctx {
   bf16* KV = nullptr;
   float* pclsh = nullptr;     // [n][H][N] per-head CLS attention of the previous layer (t)
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
-  bf16* dfull = nullptr;      // [n][T][D] Delta of reused tokens (token-indexed, bf16)
+  bf16* dfull = nullptr;      // [max_w][T][D] Delta of reused tokens (wave-local token rows, bf16)
+  int* rpos = nullptr;        // [max_w][T] compact restoration row of token w*T+i (-1: recomputed)
   bf16* patches_bf16 = nullptr;
   float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
   uint8_t* out_masks = nullptr;
@@ -78,12 +79,13 @@ struct rv_ctx {
   int wdesc_cap = 0;
   uint8_t *wmask = nullptr, *wprov = nullptr;
   int *cntR = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr;
-  bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *Ar = nullptr, *hr = nullptr;
+  bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *hr = nullptr;
   float* x1 = nullptr;
   unsigned long long* reuse_ctr = nullptr;   // [L]
   // GEMM plans (tensor maps) bound to the buffers above
   GemmPlan pe;
-  CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 128} (tcgen05 attention)
+  CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
+  CUtensorMap tmKV;                // K/V cache [n T][2 D], box {64, 1}: row gathers (tcgen05 attention)
   std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
   // ---- graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -108,12 +110,11 @@ struct rv_ctx {
   std::vector<rv_kernel_prof> prof_out;
 };
 
-enum { K_PATCH, K_PE, K_EMBED, K_SCORE, K_COMPACT, K_GATHER, K_QKV, K_RGATHER, K_ATTN, K_CLS, K_WO, K_LN2,
+enum { K_PATCH, K_PE, K_EMBED, K_SCORE, K_COMPACT, K_GATHER, K_QKV, K_ATTN, K_WO, K_LN2,
        K_FC1, K_FC2, K_R1, K_R2, K_LNPOST, K_NCLS };
 static const char* kClsName[K_NCLS] = {"patch_to_bf16", "gemm_pe", "embed_finish", "score", "compact",
-                                       "gather_ln1", "gemm_qkv", "rgather", "attention", "cls_prob",
-                                       "gemm_wo", "ln2", "gemm_fc1", "gemm_fc2", "gemm_r1", "gemm_r2",
-                                       "ln_post"};
+                                       "gather_ln1", "gemm_qkv", "attention", "gemm_wo", "ln2", "gemm_fc1",
+                                       "gemm_fc2", "gemm_r1", "gemm_r2", "ln_post"};
 
 namespace {
 
@@ -269,7 +270,8 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->KV, n * T * 2 * D);
   AL(ctx->pclsh, n * ctx->H * N);
   AL(ctx->kvsrc, n * T);
-  AL(ctx->dfull, (size_t)n * T * D);
+  AL(ctx->dfull, (size_t)max_w * T * D);
+  AL(ctx->rpos, max_w * T);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
   AL(ctx->in_patches, (size_t)n * N * ctx->pp);
   AL(ctx->in_codec, n * N);
@@ -290,16 +292,20 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->att, capC * D);
   AL(ctx->x1, capC * D);
   AL(ctx->h, capC * ctx->F);
-  AL(ctx->Ar, capR * D);
   AL(ctx->hr, capR * ctx->Hr);
   AL(ctx->reuse_ctr, 64);
 #undef AL
+  // the restoration GEMMs also read the never-written Delta rows of C tokens (results discarded)
+  if (cudaMemset(ctx->dfull, 0, (size_t)max_w * T * D * sizeof(bf16)) != cudaSuccess)
+    return fail(ctx, RV_ECUDA, "cudaMemset failed");
   ctx->n_cap = n;
   ctx->capC = capC;
   ctx->capR = capR;
   ctx->wdesc_cap = max_w;
   char e[256];
-  if (!make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 128, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+  if (!make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 64, e, sizeof e) ||
+      !make_tmap_bf16(&ctx->tmKV, ctx->KV, (long long)n * T, 2 * (int)D, 1, e, sizeof e))
+    return fail(ctx, RV_ECUDA, "%s", e);
   if (!gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e))
     return fail(ctx, RV_ECUDA, "%s", e);
   const int L = ctx->L;
@@ -316,7 +322,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
               gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
               gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e, bn_resid);
     if (ok && ctx->gates_loaded)
-      ok = gemm_make_plan(&ctx->g_r1[l], ctx->Ar, capR, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
+      ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
            gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
     if (!ok) return fail(ctx, RV_ECUDA, "%s", e);
   }
@@ -385,7 +391,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       const Wave& wv = ctx->waves[wi];
       const int n_w = wv.n_w;
       const int* wd = ctx->wdesc + (size_t)wv.off * 4;
-      const int maxC = n_w * T, maxR = n_w * N;
+      const int maxC = n_w * T;
       // a2-a3: Eq. 1-4
       r.begin(K_SCORE,l,wi);
       r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
@@ -396,10 +402,9 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
                            ctx->qoff, ctx->counts, ctx->kvsrc, ctx->reuse_ctr + l,
-                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, s),
+                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s),
             "compact");
       const int* MC = ctx->counts;
-      const int* MR = ctx->counts + 1;
       // a5: gather + LN1
       r.begin(K_GATHER,l,wi);
       r.chk(launch_gather_ln(Xin, ctx->idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, ctx->A, D, s), "gather_ln1");
@@ -417,12 +422,6 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out2_bf16 = 1;
         r.begin(K_QKV,l,wi);
         r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
-      }
-      // Eq. 8: Delta of the reused rows (written token-indexed by the score pass) -> compact
-      // restoration operand.  (a7: reused K/V are read in place through kvsrc.)
-      if (wv.any_ref) {
-        r.begin(K_RGATHER, l, wi);
-        r.chk(launch_gather_rows_bf16(ctx->dfull, ctx->idxR, MR, maxR, ctx->Ar, D, s), "rgather");
       }
       // a8: attention over all T keys; CLS row -> t for layer l+1
       r.begin(K_ATTN,l,wi);
@@ -472,16 +471,20 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         r.begin(K_FC2,l,wi);
         r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
       }
-      // a12: restoration (Eq. 9) + merge (Eq. 10, R side)
-      if (wv.any_ref) {
+      // a12: restoration (Eq. 9) + merge (Eq. 10, R side).  The score pass wrote Delta (Eq. 8)
+      // into the wave-local token rows w*T+i; R1 reads them in place over all n_w*T rows and
+      // stores only the reused rows, compacted (row map rpos; -1 for C rows): no Delta copy.
+      // R2 runs over the M_R compact rows.
+      if (wv.any_ref && !dense) {
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;
         e1.out = ctx->hr;
         e1.out_ld = Hr;
         e1.out_bf16 = 1;
+        e1.out_rows = ctx->rpos;
         r.begin(K_R1,l,wi);
-        r.chk(gemm_launch(ctx->g_r1[l], MR, 0, maxR, e1, s), "gemm_r1");
+        r.chk(gemm_launch(ctx->g_r1[l], nullptr, n_w * T, n_w * T, e1, s), "gemm_r1");
         Epi e2;
         e2.bias = w.br2;
         e2.resid = Xout;
@@ -491,7 +494,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e2.out_rows = ctx->idxR;
         e2.out_ld = D;
         r.begin(K_R2,l,wi);
-        r.chk(gemm_launch(ctx->g_r2[l], MR, 0, maxR, e2, s), "gemm_r2");
+        r.chk(gemm_launch(ctx->g_r2[l], ctx->counts + 1, 0, n_w * N, e2, s), "gemm_r2");
       }
     }
   }
@@ -932,9 +935,7 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
       case K_COMPACT: a.bytes += nw * T * 2.0 + (MC + 2 * MR) * 4.0; break;
       case K_GATHER: a.bytes += MC * (D * 4.0 + D * 2.0 + 4.0); break;
       case K_QKV: a.flops += 2.0 * MC * 3 * D * D; a.bytes += MC * (D * 2.0 + 3 * D * 2.0) + 3 * D * D * 2.0; break;
-      case K_RGATHER: a.bytes += MR * (D * 2.0 + D * 2.0 + 4.0); break;
       case K_ATTN: a.flops += 4.0 * MC * T * D; a.bytes += MC * D * 4.0 + nw * T * 2 * D * 2.0; break;
-      case K_CLS: a.bytes += nw * (T * D * 2.0 + D * 2.0 + N * 4.0); break;
       case K_WO: a.flops += 2.0 * MC * D * D; a.bytes += MC * (D * 2.0 + D * 4.0 + D * 4.0) + D * D * 2.0; break;
       case K_LN2: a.bytes += MC * (D * 4.0 + D * 2.0); break;
       case K_FC1: a.flops += 2.0 * MC * F * D; a.bytes += MC * (D * 2.0 + F * 2.0) + F * D * 2.0; break;
@@ -969,7 +970,7 @@ rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const
   if (!ctx) return RV_ECONTRACT;
   CK(cudaSetDevice(ctx->device));
   CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntR, idxC, idxR, provrow, qoff, counts, nullptr, nullptr, nullptr,
-                    (cudaStream_t)stream));
+                    nullptr, (cudaStream_t)stream));
   return RV_OK;
 }
 
@@ -999,11 +1000,18 @@ rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, con
   if (q_rows < 1 || !q || !KV || !out) return fail(ctx, RV_ECONTRACT, "rv_stage_attention: bad arguments");
   CK(cudaSetDevice(ctx->device));
   if (use_tc && !attn_tc_supported(ctx->T, ctx->D, ctx->H))
-    return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and 128 <= T <= 320");
+    return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and T - 1 <= 256");
   if (use_tc) {
-    CUtensorMap tm;
+    // K/V rows the wave can address: slots 0..max(slot); the tensor map needs the extent
+    std::vector<int32_t> wd((size_t)n_w * 4);
+    CK(cudaMemcpy(wd.data(), wdesc, wd.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    long long slots = 0;
+    for (int w = 0; w < n_w; ++w) slots = std::max<long long>(slots, wd[(size_t)w * 4] + 1LL);
+    CUtensorMap tm, tkv;
     char e[256];
-    if (!make_tmap_bf16(&tm, q, q_rows, ctx->D, 128, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+    if (!make_tmap_bf16(&tm, q, q_rows, ctx->D, 64, e, sizeof e) ||
+        !make_tmap_bf16(&tkv, KV, slots * ctx->T, 2 * ctx->D, 1, e, sizeof e))
+      return fail(ctx, RV_ECUDA, "%s", e);
     CK(launch_attention_tc(tm, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
                            (cudaStream_t)stream));
   } else {

@@ -11,7 +11,8 @@ namespace rv {
 
 // ---------------------------------------------------------------- GEMM epilogue (k_gemm.cu)
 // out[orow(m)][n] = act(acc[m][n] + bias[n]) + resid[rrow(m)][n]   (fp32 residual)
-// orow(m) = out_rows ? out_rows[m] : m + (row_div ? m / row_div : 0) + row_add
+// orow(m) = out_rows ? out_rows[m] : m + (row_div ? m / row_div : 0) + row_add; orow(m) < 0: row m
+// is computed but not stored (restoration GEMM R1 over the wave's token rows)
 // Columns n >= split go to out2 (column n - split) with rows out2_rows[m].
 struct Epi {
   const float* bias = nullptr;
@@ -54,11 +55,6 @@ cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, co
                                 float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s);
 cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
                              const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
-cudaError_t launch_rgather(const float* X, const int* idxR, const int* provrow, const int* count, int max_rows,
-                           bf16* Ar, int D, cudaStream_t s);
-// Ar[m] = dfull[idxR[m]] (bf16 rows of D): the restoration operand from the score pass's Delta
-cudaError_t launch_gather_rows_bf16(const bf16* src, const int* rows, const int* count, int max_rows, bf16* dst,
-                                   int D, cudaStream_t s);
 cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
                            cudaStream_t s);
 
@@ -69,7 +65,7 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
                          int* cntR, bf16* dfull, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, cudaStream_t s);
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s);
 
 // 2D bf16 tensor map, box {64 cols, box_rows}, SWIZZLE_128B (k_gemm.cu)
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, int box_rows, char* err,
