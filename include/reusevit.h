@@ -95,8 +95,8 @@ typedef struct {
 #define RV_FORCE_MASKS 4u  /* masks is an INPUT [n][L][N]: forced reuse map (diagnostic, Q18)   */
 #define RV_NO_GRAPH 8u     /* launch kernels directly instead of through a cached CUDA graph    */
 #define RV_PROFILE 16u     /* time every kernel launch with CUDA events (see rv_profile)         */
-#define RV_ATTN_TC 32u     /* attention on tcgen05/TMEM (k_attn_tc.cu, d_h = 64, T - 1 <= 256)
-                              instead of the default mma.sync kernel (k_attn.cu)                 */
+#define RV_ATTN_SYNC 32u   /* attention on the mma.sync kernel (k_attn.cu) even where the default
+                              tcgen05/TMEM kernel (k_attn_tc.cu: d_h = 64, T - 1 <= 256) applies */
 
 /* Per-kernel-class profile of the last RV_PROFILE embed (rv_profile). */
 typedef struct {

@@ -57,11 +57,14 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
  * out [M_C][D] bf16 = softmax(q K^T / sqrt(dh)) V per head; pcls [slots][H][N] fp32 (or
  * NULL) = per-head CLS softmax row over the patch keys; its head mean is t for the next
  * layer.  q_rows = allocated rows of q (>= qoff[n_w]; the tcgen05 path
- * reads q with TMA in 128-row tiles).  use_tc selects the tcgen05/TMEM kernel (d_h = 64,
- * T - 1 <= 256; RV_ECONTRACT otherwise), else the mma.sync kernel (any supported shape). */
+ * reads q with TMA in 64-row tiles).  kvsrc [slots][T] int32 (or NULL = identity) is the
+ * reuse-cache row table of a7: key j of the frame in slot s is row kvsrc[s*T + j] of KV.
+ * use_tc selects the tcgen05/TMEM kernel (d_h = 64, T - 1 <= 256; RV_ECONTRACT otherwise),
+ * else the mma.sync kernel (any supported shape). */
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
                              const int32_t* qoff, const void* q, int32_t q_rows, const void* KV,
-                             void* out, float* pcls, int32_t use_tc, void* stream);
+                             const int32_t* kvsrc, void* out, float* pcls, int32_t use_tc,
+                             void* stream);
 
 #ifdef __cplusplus
 }

@@ -427,8 +427,8 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       r.begin(K_ATTN,l,wi);
       {
         float* pcl = (!dense && l + 1 < L) ? ctx->pclsh : nullptr;
-        if ((flags & RV_ATTN_TC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM kernel (opt-in)
-          r.chk(launch_attention_tc(ctx->tmQ, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
+        if (!(flags & RV_ATTN_SYNC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM kernel (default)
+          r.chk(launch_attention_tc(ctx->tmQ, ctx->tmKV, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
         else
           r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
@@ -994,8 +994,8 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
 }
 
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const int32_t* qoff, const void* q,
-                             int32_t q_rows, const void* KV, void* out, float* pcls, int32_t use_tc,
-                             void* stream) {
+                             int32_t q_rows, const void* KV, const int32_t* kvsrc, void* out, float* pcls,
+                             int32_t use_tc, void* stream) {
   if (!ctx) return RV_ECONTRACT;
   if (q_rows < 1 || !q || !KV || !out) return fail(ctx, RV_ECONTRACT, "rv_stage_attention: bad arguments");
   CK(cudaSetDevice(ctx->device));
@@ -1012,10 +1012,10 @@ rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, con
     if (!make_tmap_bf16(&tm, q, q_rows, ctx->D, 64, e, sizeof e) ||
         !make_tmap_bf16(&tkv, KV, slots * ctx->T, 2 * ctx->D, 1, e, sizeof e))
       return fail(ctx, RV_ECUDA, "%s", e);
-    CK(launch_attention_tc(tm, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
+    CK(launch_attention_tc(tm, tkv, (const bf16*)KV, kvsrc, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T, ctx->D, ctx->H,
                            (cudaStream_t)stream));
   } else {
-    CK(launch_attention((const bf16*)q, (const bf16*)KV, nullptr, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T,
+    CK(launch_attention((const bf16*)q, (const bf16*)KV, kvsrc, (bf16*)out, wdesc, qoff, pcls, n_w, ctx->T,
                         ctx->D, ctx->H, (cudaStream_t)stream));
   }
   return RV_OK;

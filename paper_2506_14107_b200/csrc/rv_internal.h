@@ -73,7 +73,8 @@ bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, i
 
 // ---------------------------------------------------------------- attention (k_attn_tc.cu, k_attn.cu)
 bool attn_tc_supported(int T, int D, int H);
-cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const bf16* KV, const int* kvsrc, bf16* out,
+cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const bf16* KV, const int* kvsrc,
+                                bf16* out,
                                 const int* wdesc, const int* qoff, float* pclsh, int n_w, int T, int D, int H,
                                 cudaStream_t s);
 cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,

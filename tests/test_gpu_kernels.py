@@ -106,6 +106,55 @@ def test_attention_vs_torch(dev, cfgname, use_tc):
         assert (pcls[s].cpu() - tref).abs().max().item() < 1e-4
 
 
+@pytest.mark.parametrize("cfgname,use_tc", [("b16", False), ("l14", False), ("b16", True), ("l14", True)])
+def test_attention_wave_kvsrc(dev, cfgname, use_tc):
+    """A level-wave-sized launch: 300 frames in shuffled slots, ragged query counts (1 .. T,
+    mostly the 30-70 of the paper's reuse rates), K/V rows read through a random reuse-cache
+    table (a7: reused tokens point at another slot's row of the same token), vs torch fp32."""
+    cfg = synth.CONFIGS[cfgname]
+    m, _, _ = _model(cfg, gates=False)
+    T, D, H, dh = cfg.T, cfg.dim, cfg.heads, cfg.dh
+    rng = np.random.default_rng(7)
+    n_w = 300
+    slot_of = rng.permutation(n_w).astype(np.int32)
+    nq = rng.integers(30, 71, n_w)
+    nq[::20] = T
+    nq[5::37] = 1
+    nq[7::41] = 64
+    nq[9::43] = 65
+    qoff = np.concatenate([[0], np.cumsum(nq)]).astype(np.int32)
+    kvsrc = np.arange(n_w * T, dtype=np.int32).reshape(n_w, T)
+    other = rng.integers(0, n_w, (n_w, T))
+    reuse = rng.random((n_w, T)) < 0.7
+    reuse[:, 0] = False
+    kvsrc[reuse] = (other * T + np.arange(T)[None, :])[reuse]
+    g = torch.Generator(device=dev).manual_seed(3)
+    q = torch.randn(int(qoff[-1]), D, device=dev, generator=g).to(torch.bfloat16)
+    KV = torch.randn(n_w * T, 2 * D, device=dev, generator=g).to(torch.bfloat16)
+    wdesc = np.zeros((n_w, 4), np.int32)
+    wdesc[:, 0] = slot_of
+    out = torch.zeros((int(qoff[-1]), D), dtype=torch.bfloat16, device=dev)
+    pcls = torch.zeros((n_w, H, cfg.N), dtype=torch.float32, device=dev)
+    kv_d = torch.from_numpy(kvsrc).to(dev)
+    m.stage_attention(torch.from_numpy(wdesc).to(dev), torch.from_numpy(qoff).to(dev), q, KV, out, pcls,
+                      torch.cuda.current_stream(), use_tc=use_tc, kvsrc=kv_d)
+    torch.cuda.synchronize()
+    worst, worst_p = 0.0, 0.0
+    for w in range(n_w):
+        s = int(slot_of[w])
+        rows = kv_d[s].long()
+        Kf = KV[rows, :D].float().reshape(T, H, dh).transpose(0, 1)
+        Vf = KV[rows, D:].float().reshape(T, H, dh).transpose(0, 1)
+        qf = q[qoff[w]:qoff[w + 1]].float().reshape(-1, H, dh).transpose(0, 1)
+        P = torch.softmax(qf @ Kf.transpose(1, 2) / dh ** 0.5, dim=-1)
+        ref = (P @ Vf).transpose(0, 1).reshape(-1, D)
+        got = out[qoff[w]:qoff[w + 1]].float()
+        worst = max(worst, (got - ref).abs().max().item() / (1 + ref.abs().max().item()))
+        worst_p = max(worst_p, (pcls[s] - P[:, 0, 1:]).abs().max().item())
+    assert worst < 2e-2, worst
+    assert worst_p < 1e-4, worst_p
+
+
 # ------------------------------------------------------------------------- score (teacher forced)
 @pytest.mark.parametrize("cfgname,mode,n", [("tiny", "continuous", 8), ("b16", "bimodal", 9), ("b16", "continuous", 9)])
 def test_score_teacher_forced(dev, cfgname, mode, n):

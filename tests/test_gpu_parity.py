@@ -41,21 +41,22 @@ def build(cfg, **gk):
 
 
 CASES = [
-    # cfg, frames on GPU, frames checked by the oracle (prefix-closed), motion p, mode[, attn_tc]
+    # cfg, frames on GPU, frames checked by the oracle (prefix-closed), motion p, mode[, "sync"]
+    # (default attention: tcgen05 where d_h = 64 and T - 1 <= 256; "sync": the mma.sync kernel)
     ("tiny", 8, 8, 0.3, "bimodal"),
     ("tiny", 41, 41, 0.2, "bimodal"),
     ("b16", 32, 32, 0.3, "bimodal"),
     ("b16", 32, 32, 0.1, "bimodal"),
     ("l14", 64, 21, 0.2, "bimodal"),
-    ("b16", 32, 32, 0.3, "bimodal", True),
-    ("l14", 64, 21, 0.2, "bimodal", True),
+    ("b16", 32, 32, 0.3, "bimodal", "sync"),
+    ("l14", 64, 21, 0.2, "bimodal", "sync"),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-n{c[1]}-p{c[3]}" + ("-tc" if len(c) > 5 else "") for c in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-n{c[1]}-p{c[3]}" + ("-sync" if len(c) > 5 else "") for c in CASES])
 def test_embed_parity(cuda_ok, case):
     cfgname, n, n_check, p, mode = case[:5]
-    attn_tc = len(case) > 5 and case[5]
+    attn_tc = not (len(case) > 5 and case[5] == "sync")
     cfg = synth.CONFIGS[cfgname]
     m, W, G = build(cfg)
     x, c = synth.make_video(cfg, n, p, seed=2000 + n)

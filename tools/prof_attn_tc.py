@@ -1,4 +1,4 @@
-"""One ReuseViT embed with the tcgen05 attention (RV_ATTN_TC) for ncu."""
+"""One ReuseViT embed (tcgen05 attention, the default) for ncu."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
