@@ -71,8 +71,8 @@ def test_gemm_row_position_invariance(dev):
 
 
 # ------------------------------------------------------------------------- attention
-@pytest.mark.parametrize("cfgname,use_tc", [("tiny", False), ("b16", False), ("l14", False), ("b16", True),
-                                            ("l14", True)])
+@pytest.mark.parametrize("cfgname,use_tc", [("tiny", False), ("b16", False), ("l14", False), ("l14_336", False),
+                                            ("b16", True), ("l14", True)])
 def test_attention_vs_torch(dev, cfgname, use_tc):
     cfg = synth.CONFIGS[cfgname]
     m, _, _ = _model(cfg, gates=False)
@@ -106,7 +106,8 @@ def test_attention_vs_torch(dev, cfgname, use_tc):
         assert (pcls[s].cpu() - tref).abs().max().item() < 1e-4
 
 
-@pytest.mark.parametrize("cfgname,use_tc", [("b16", False), ("l14", False), ("b16", True), ("l14", True)])
+@pytest.mark.parametrize("cfgname,use_tc", [("b16", False), ("l14", False), ("l14_336", False), ("b16", True),
+                                            ("l14", True)])
 def test_attention_wave_kvsrc(dev, cfgname, use_tc):
     """A level-wave-sized launch: 300 frames in shuffled slots, ragged query counts (1 .. T,
     mostly the 30-70 of the paper's reuse rates), K/V rows read through a random reuse-cache

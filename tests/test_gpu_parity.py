@@ -48,6 +48,7 @@ CASES = [
     ("b16", 32, 32, 0.3, "bimodal"),
     ("b16", 32, 32, 0.1, "bimodal"),
     ("l14", 64, 21, 0.2, "bimodal"),
+    ("l14_336", 24, 9, 0.2, "bimodal"),          # C5 shape: T = 577 (mma.sync attention)
     ("b16", 32, 32, 0.3, "bimodal", "sync"),
     ("l14", 64, 21, 0.2, "bimodal", "sync"),
 ]
