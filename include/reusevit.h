@@ -95,6 +95,9 @@ typedef struct {
 #define RV_FORCE_MASKS 4u  /* masks is an INPUT [n][L][N]: forced reuse map (diagnostic, Q18)   */
 #define RV_NO_GRAPH 8u     /* launch kernels directly instead of through a cached CUDA graph    */
 #define RV_PROFILE 16u     /* time every kernel launch with CUDA events (see rv_profile)         */
+#define RV_WAVE_FRAME 64u  /* ablation (SURVEY §8(d) ladder step 2): every frame is its own wave,
+                              i.e. per-frame compaction instead of level-batched cross-frame
+                              compaction (results identical, only the batching differs)         */
 #define RV_ATTN_SYNC 32u   /* attention on the mma.sync kernel (k_attn.cu) even where the default
                               tcgen05/TMEM kernel (k_attn_tc.cu: d_h = 64, T - 1 <= 256) applies */
 

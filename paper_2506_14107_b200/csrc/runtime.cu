@@ -706,7 +706,7 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   const int n = plan->n, T = ctx->T, N = ctx->N, L = ctx->L, D = ctx->D;
   // ---- level-waves: frames of equal level in computation order; dense = one level.
   // Large levels are split into waves of at most kMaxWave frames (bounds the wave buffers).
-  const int kMaxWave = 1536;
+  const int kMaxWave = (flags & RV_WAVE_FRAME) ? 1 : 1536;
   std::vector<std::vector<int>> levels;
   for (int k = 0; k < n; ++k) {
     const int f = plan->order[k];

@@ -145,6 +145,26 @@ def test_determinism_graph_and_host_paths(cuda_ok):
     assert st["ms_total"] > 0 and st["n_launches"] > 0
 
 
+@pytest.mark.parametrize("cfgname", ["b16", "l14"])
+def test_per_frame_waves_equal_level_waves(cuda_ok, cfgname):
+    """RV_WAVE_FRAME (ablation ladder step 2: per-frame compaction) changes only the batching
+    (SURVEY Q20 math-neutral scheduling): kernels are batch-invariant, so results are bitwise
+    equal to the level-batched default; the same for the mma.sync attention."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 21, 0.3, seed=12)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    Z1, M1, _, _ = m.embed(xd, cd)
+    Z2, M2, _, _ = m.embed(xd, cd, per_frame_waves=True)
+    torch.cuda.synchronize()
+    assert torch.equal(M1, M2)
+    assert torch.equal(Z1, Z2)
+    Z3, M3, _, _ = m.embed(xd, cd, attn_tc=False)
+    Z4, M4, _, _ = m.embed(xd, cd, attn_tc=False, per_frame_waves=True)
+    torch.cuda.synchronize()
+    assert torch.equal(M3, M4) and torch.equal(Z3, Z4)
+
+
 def test_duplicate_frame_reuses_everything(cuda_ok):
     cfg = synth.CONFIGS["b16"]
     from paper_2506_14107_b200 import ReuseViT
