@@ -45,15 +45,23 @@ constexpr int A8_MAX_TILES = 5;                // T <= 257 -> <= 257 compact que
 constexpr int A8_NKT = 2;                      // K tile ring slots
 constexpr int A8_NVT = 3;                      // V tile ring slots
 constexpr int A8_NT = A8_NKT + A8_NVT;
-constexpr int A8_NQ = 4;                       // Q ring slots = items in flight = TMEM regions
+#ifndef A8_NQ_SLOTS
+#define A8_NQ_SLOTS 4
+#endif
+constexpr int A8_NQ = A8_NQ_SLOTS;             // Q ring slots (items the loader may run ahead)
 constexpr uint32_t A8_TILE = A8_MAXK * 128;    // 256 keys x 128 B
-constexpr uint32_t A8_QSLOT = 8192 + 2048;     // Q tile, k_cls row (+8192), v_cls row (+9216)
+// Q tile, then the CLS key's K row at +8192 (row 0 of a 1 KB swizzle atom: unswizzled) and its
+// V row at +8320 (row 1: 16 B chunk c stored at chunk c ^ 1)
+constexpr uint32_t A8_QSLOT = 8192 + 1024;
 constexpr uint32_t A8_QTX = 8192 + 256;        // bytes the Q slot's TMA deliver
 constexpr uint32_t A8_RING = A8_NQ * A8_QSLOT; // tile ring offset (1 KB aligned)
 constexpr uint32_t A8_ROWS = A8_RING + A8_NT * A8_TILE;   // int32 [A8_NQ][256] K/V source rows
 constexpr uint32_t A8_META = A8_ROWS + A8_NQ * A8_MAXK * 4;
 constexpr uint32_t A8_TMEM_COLS = 512;
 constexpr uint32_t A8_O_OFF = 128;
+#ifndef A8_POLL_SLEEP
+#define A8_POLL_SLEEP 0
+#endif
 #ifndef A8_DEFER_EPI
 #define A8_DEFER_EPI 0
 #endif
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
         mbar_expect_tx(&q_full[qs], A8_QTX);
         tma_2d(sQ(qs), &tmQ, c_h * 64, c_q0, &q_full[qs]);
         tma_2d(sQ(qs) + 8192, &tmKV, c_h * 64, c_sl * T, &q_full[qs]);       // k_cls
-        tma_2d(sQ(qs) + 9216, &tmKV, D + c_h * 64, c_sl * T, &q_full[qs]);   // v_cls
+        tma_2d(sQ(qs) + 8320, &tmKV, D + c_h * 64, c_sl * T, &q_full[qs]);   // v_cls
       }
       int* rb = rowsbuf + qs * A8_MAXK;
       *reinterpret_cast<int4*>(rb + 128 * half + 4 * lane) = make_int4(rows[0], rows[1], rows[2], rows[3]);
@@ -412,6 +420,7 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       uint32_t kseq = 0, vseq = 0;
       int js = 0, jp = 0, j_end = 0x7fffffff;
       while (jp < j_end) {
+        const int js0 = js, jp0 = jp;
         if (js < j_end) {
           const int qs = js % A8_NQ;
           if (mbar_test(&q_full[qs], (js / A8_NQ) & 1)) {
@@ -453,6 +462,11 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
             ++jp;
           }
         }
+#if A8_POLL_SLEEP > 0
+        // nothing issuable: back off so the polling does not steal issue slots from the softmax
+        // warps sharing this SM sub-partition
+        if (js == js0 && jp == jp0) __nanosleep(A8_POLL_SLEEP);
+#endif
       }
     }
   } else if (warp < A8_SMX0) {
@@ -579,11 +593,11 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
         tld_wait();
         if (row < m.nrows) {
           const float il = 1.f / l;
-          const uint8_t* vc = sm + (size_t)qs * A8_QSLOT + 9216 + hl * 64;
+          const uint8_t* vc = sm + (size_t)qs * A8_QSLOT + 8320;
           bf16* dst = out + (long long)(m.q0 + row) * D + m.h * 64 + hl * 32;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint4 va = *reinterpret_cast<const uint4*>(vc + c * 16);
+            const uint4 va = *reinterpret_cast<const uint4*>(vc + (((hl * 4 + c) ^ 1) << 4));
             const uint32_t vw[4] = {va.x, va.y, va.z, va.w};
             uint32_t u[4];
 #pragma unroll
