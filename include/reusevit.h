@@ -173,6 +173,23 @@ const char* rv_status_string(rv_status s);
 /* Free every device and host resource of ctx (NULL is a no-op). */
 void rv_destroy(rv_ctx* ctx);
 
+/* ---- Embedding store query (paper §6.1: embeddings are
+ * cached per frame as fp16 (~2 KB each at D = 1024) and retrieved by similarity; on a miss the
+ * frames are embedded).  No context: plain device buffers on `stream`.
+ *
+ * rv_f32_to_f16: dst[i] = fp16(src[i]) (round to nearest even), count elements, device
+ *   pointers.  RV_ECONTRACT on a negative count or NULL buffers, RV_ECUDA on a launch error.
+ * rv_topk_cosine: emb16 [n][D] fp16, q [nq][D] fp32, scores_tmp [nq][n] fp32 scratch (its
+ *   contents are destroyed), out_idx [nq][k] int32, out_score [nq][k] fp32, all device.  Row t
+ *   of query i is the stored record of t-th highest cosine similarity cos(q_i, e_r) =
+ *   q.e / (|q| |e|) (0 when either norm is 0), descending; equal scores are ordered by
+ *   the lower record index (SPEC embed-store: ties by (video_id, frame_index), i.e. the store's
+ *   record order).  k > n: entries past n are -1 / -inf.  D % 8 == 0.  RV_ECONTRACT on bad
+ *   arguments, RV_ECUDA on a launch error; results are complete in stream order. */
+rv_status rv_f32_to_f16(const float* src, void* dst, int64_t count, void* stream);
+rv_status rv_topk_cosine(const void* emb16, int32_t n, int32_t D, const float* q, int32_t nq, int32_t k,
+                         float* scores_tmp, int32_t* out_idx, float* out_score, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,3 +21,4 @@ from .reusevit_ref import (  # noqa: F401
     similarity, decision_mlp, restoration_mlp, reuse_embed, dense_embed,
     compaction_indices, flops_per_frame, reuse_rates,
 )
+from .store_ref import to_fp16, cosine_scores, topk_cosine, storage_bytes_per_second  # noqa: F401

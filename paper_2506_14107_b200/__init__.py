@@ -5,3 +5,4 @@ ctypes binding.  Build with ``__graft_entry__.build()``.  See DESIGN.md.
 """
 from .api import ReuseViT, gate_blob_floats, plan_check, plan_gop, vit_blob_floats  # noqa: F401
 from ._lib import ReuseViTError, load_library  # noqa: F401
+from .store import EmbeddingStore  # noqa: F401

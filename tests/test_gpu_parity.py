@@ -145,6 +145,25 @@ def test_determinism_graph_and_host_paths(cuda_ok):
     assert st["ms_total"] > 0 and st["n_launches"] > 0
 
 
+@pytest.mark.parametrize("cfgname,n,n_check", [("tiny", 25, 25), ("b16", 24, 24)])
+def test_streaming_mode_parity(cuda_ok, cfgname, n, n_check):
+    """SURVEY §8(f) NEXT-3, low-latency mode: reordering off, every frame is a P
+    frame referencing its predecessor (I every 20, one dependency level per frame) — vs the
+    fp64 oracle run on the same all-P plan."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, n, 0.3, seed=31)
+    plan = oracle.plan_gop(n, reorder=False)
+    Z, M, _, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), plan, reorder=False)
+    torch.cuda.synchronize()
+    frames = list(range(n_check))
+    ref = oracle.reuse_embed(cfg, W, G, x, c, plan, frames=frames)
+    err, cos = metrics(Z.cpu().numpy()[frames], ref["Z"][frames])
+    agree, cnt = mask_agreement(M.cpu().numpy(), ref, frames)
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and agree >= 0.999, (err.max(), cos.min(), agree)
+    assert st["n_levels"] >= 20 and st["reuse_all"] > 0.2
+
+
 @pytest.mark.parametrize("cfgname", ["b16", "l14"])
 def test_per_frame_waves_equal_level_waves(cuda_ok, cfgname):
     """RV_WAVE_FRAME (ablation ladder step 2: per-frame compaction) changes only the batching

@@ -356,3 +356,47 @@ def test_reuse_rates():
     assert oracle.reuse_rates(M, types, T) == (0.0, 0.0)
     M[1:, :, :2] = 1
     assert oracle.reuse_rates(M, types, T)[0] == 0.5
+
+
+# ------------------------------------------------------------------ embedding store (NEXT-4)
+def test_store_topk_matches_exhaustive_scan():
+    """S:530 'k=1 on 100 random records -> matches exhaustive scan': pure-Python loops."""
+    rng = np.random.default_rng(5)
+    E16 = oracle.to_fp16(rng.standard_normal((100, 24)))
+    Q = rng.standard_normal((4, 24))
+    idx, sc = oracle.topk_cosine(E16, Q, 3)
+    for i in range(4):
+        scores = []
+        for r in range(100):
+            e = [float(v) for v in E16[r]]
+            q = [float(v) for v in Q[i]]
+            dot = sum(a * b for a, b in zip(e, q))
+            den = (sum(a * a for a in e) ** 0.5) * (sum(b * b for b in q) ** 0.5)
+            scores.append((-(dot / den), r))
+        best = sorted(scores)[:3]
+        assert [r for _, r in best] == list(idx[i])
+        assert np.allclose([-s for s, _ in best], sc[i], rtol=0, atol=1e-12)
+
+
+def test_store_topk_examples():
+    """S:529 query = stored vector -> that record first with score ~1; S:531 orthogonal query
+    -> scores ~0 in index order; zero vector -> cosine 0; k > n returns all."""
+    E = np.zeros((5, 8))
+    E[np.arange(5), np.arange(5)] = 1.0
+    E16 = oracle.to_fp16(E)
+    idx, sc = oracle.topk_cosine(E16, E[3], 2)
+    assert idx[0, 0] == 3 and abs(sc[0, 0] - 1.0) < 1e-12
+    q = np.zeros(8)
+    q[7] = 1.0                                        # orthogonal to every record
+    idx, sc = oracle.topk_cosine(E16, q, 5)
+    assert list(idx[0]) == [0, 1, 2, 3, 4] and np.all(sc == 0)
+    idx, sc = oracle.topk_cosine(E16, np.zeros(8), 2)
+    assert list(idx[0]) == [0, 1] and np.all(sc == 0)
+    idx, sc = oracle.topk_cosine(E16, E[0], 7)
+    assert list(idx[0, 5:]) == [-1, -1] and np.all(np.isinf(sc[0, 5:]))
+
+
+def test_store_storage_arithmetic():
+    """1024-dim fp16 at 2 FPS = 4 KB/s ~ 0.64% of a ~625 KB/s Full-HD H.264 stream."""
+    bps = oracle.storage_bytes_per_second(1024, 2.0)
+    assert bps == 4096 and abs(bps / (625 * 1024) * 100 - 0.64) < 0.005
