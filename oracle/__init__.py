@@ -22,3 +22,4 @@ from .reusevit_ref import (  # noqa: F401
     compaction_indices, flops_per_frame, reuse_rates,
 )
 from .store_ref import to_fp16, cosine_scores, topk_cosine, storage_bytes_per_second  # noqa: F401
+from .chain_ref import reuse_embed_chain  # noqa: F401

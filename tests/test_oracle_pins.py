@@ -400,3 +400,60 @@ def test_store_storage_arithmetic():
     """1024-dim fp16 at 2 FPS = 4 KB/s ~ 0.64% of a ~625 KB/s Full-HD H.264 stream."""
     bps = oracle.storage_bytes_per_second(1024, 2.0)
     assert bps == 4096 and abs(bps / (625 * 1024) * 100 - 0.64) < 0.005
+
+
+# ------------------------------------------------------------------ SPEC chain variant (NEXT-1)
+from tests import bruteforce_chain  # noqa: E402
+
+
+@pytest.mark.parametrize("mode,p,seed", [("bimodal", 0.3, 2000), ("continuous", 0.0, 2001)])
+def test_chain_oracle_equals_bruteforce_tiny(mode, p, seed):
+    """Chain variant (FFN_l -> QKV_{l+1} gated, dense attention + W_o, S:218-220 / S:271-272) vs
+    the pure-Python token-by-token implementation: embeddings and masks."""
+    tau = 0.7 if mode == "bimodal" else 0.3
+    W, G, x, c = _tiny_inputs(n=5, p=p, seed=seed, mode=mode, tau=tau)
+    plan = oracle.plan_gop(5)
+    out = oracle.reuse_embed_chain(TINY, W, G, x, c, plan)
+    Zb, Mb = bruteforce_chain.run(TINY, W, G, x, c, plan)
+    M = out["M"]
+    assert 0 < M.sum() < M[plan["type"] != 0].size, "test needs a mix of reuse and recompute"
+    for f in range(5):
+        np.testing.assert_allclose(out["Z"][f], Zb[f], rtol=0, atol=1e-10)
+        assert M[f].tolist() == Mb[f]
+
+
+def test_chain_oracle_force_masks_bruteforce():
+    W, G, x, c = _tiny_inputs(n=5, p=0.5, seed=2003)
+    plan = oracle.plan_gop(5)
+    rng = np.random.default_rng(6)
+    fm = (rng.random((5, TINY.layers, TINY.N)) < 0.5).astype(np.uint8)
+    fm[plan["type"] == 0] = 0
+    out = oracle.reuse_embed_chain(TINY, W, G, x, c, plan, force_masks=fm)
+    Zb, Mb = bruteforce_chain.run(TINY, W, G, x, c, plan, force_masks=fm)
+    assert np.array_equal(out["M"], fm)
+    for f in range(5):
+        np.testing.assert_allclose(out["Z"][f], Zb[f], rtol=0, atol=1e-10)
+
+
+def test_chain_oracle_zero_masks_equal_torch_library():
+    """S:264 exactness at zero reuse, for the chain variant: forced M = 0 -> plain ViT."""
+    cfg = TINY
+    W, G, x, c = _tiny_inputs(n=5, p=0.5, seed=2004)
+    plan = oracle.plan_gop(5)
+    fm = np.zeros((5, cfg.layers, cfg.N), np.uint8)
+    out = oracle.reuse_embed_chain(cfg, W, G, x, c, plan, force_masks=fm)
+    np.testing.assert_allclose(out["Z"], _torch_vit(cfg, W, x), rtol=0, atol=1e-10)
+
+
+def test_chain_duplicate_frame_invariant():
+    """S:260/S:265 in the chain variant: a P-frame identical to its reference reuses every
+    patch token (x' identical -> s = 1) and, with zero restoration biases, Z_f = Z_ref."""
+    cfg = TINY
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=False)
+    x, c = synth.make_video(cfg, 5, 0.5, duplicate_of={4: 0})
+    c[4] = 0.0
+    plan = oracle.plan_gop(5)
+    out = oracle.reuse_embed_chain(cfg, W, G, x, c, plan)
+    assert out["M"][4].all()
+    np.testing.assert_allclose(out["Z"][4], out["Z"][0], rtol=0, atol=1e-12)
