@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--attn-sync", action="store_true", help="mma.sync attention kernel (RV_ATTN_SYNC) instead of tcgen05")
+    ap.add_argument("--chain", action="store_true", help="SPEC chain variant (RV_CHAIN, SURVEY NEXT-1) instead of D1")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -260,7 +261,8 @@ def main():
         p_msk = torch.zeros((n_max, L * N), dtype=torch.uint8, device=dev)
 
     def step(profile):
-        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync)
+        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync,
+                      chain=args.chain)
         st = m.wait()
         if world > 1:     # NCCL over NVLink only to gather embeddings + masks
             p_emb[:n_loc].copy_(emb)
@@ -414,7 +416,8 @@ def main():
                        "model": "ViT-L/14 (random init) + structured gates", "frames": n_total,
                        "frames_per_gpu": n_own, "halo_frames": n_loc - n_own, "seq_len": T,
                        "parallelism": f"frame-group dp{world}", "l2": "inputs 4.3 GB fp32 > 126 MB L2, no flush",
-                       "compute": "bf16 operands, fp32 accumulate, fp32 residual"},
+                       "compute": "bf16 operands, fp32 accumulate, fp32 residual",
+                       "variant": "SPEC chain (RV_CHAIN)" if args.chain else "D1 layer-gated (default)"},
             "reuse": {"reuse_all": stats["reuse_all"], "reuse_nonI": stats["reuse_nonI"]},
             "flops_exec_per_step": stats["flops_exec"], "flops_dense_per_step": stats["flops_dense"],
             "tc_frac_exec": stats["flops_exec"] / (ms / 1e3) / 1e12 / peaks["tc_sustained"],

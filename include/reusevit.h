@@ -98,6 +98,9 @@ typedef struct {
 #define RV_WAVE_FRAME 64u  /* ablation (SURVEY §8(d) ladder step 2): every frame is its own wave,
                               i.e. per-frame compaction instead of level-batched cross-frame
                               compaction (results identical, only the batching differs)         */
+#define RV_CHAIN 128u      /* SPEC chain variant: the
+                              decision on the FFN input x'_l gates FFN_l -> QKV_{l+1}; attention
+                              and W_o dense for all tokens (mma.sync attention path)            */
 #define RV_ATTN_SYNC 32u   /* attention on the mma.sync kernel (k_attn.cu) even where the default
                               tcgen05/TMEM kernel (k_attn_tc.cu: d_h = 64, T - 1 <= 256) applies */
 

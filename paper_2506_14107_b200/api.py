@@ -16,7 +16,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import (RV_ATTN_SYNC, RV_WAVE_FRAME, RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_NO_GRAPH, RV_PROFILE, RvConfig,
+from ._lib import (RV_ATTN_SYNC, RV_CHAIN, RV_WAVE_FRAME, RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_NO_GRAPH, RV_PROFILE, RvConfig,
                    RvKernelProf, RvPlan, RvStats, check, load_library)
 
 __all__ = ["ReuseViT", "plan_gop", "plan_check", "vit_blob_floats", "gate_blob_floats"]
@@ -116,7 +116,7 @@ class ReuseViT:
                     reorder: bool = True, dense: bool = False, force_masks=None, want_masks: bool = True,
                     want_scores: bool = False, stream=None, graph: bool = True, out=None,
                     profile: bool = False, attn_tc: bool = True,
-                    per_frame_waves: bool = False):
+                    per_frame_waves: bool = False, chain: bool = False):
         """Enqueue one embed; returns a handle for ``wait``.  ``out`` optionally supplies the
         output buffers (emb, masks, scores) to reuse across calls (same pointers -> the
         cached CUDA graph is replayed)."""
@@ -129,7 +129,7 @@ class ReuseViT:
         device_path = isinstance(patches, torch.Tensor) and patches.is_cuda
         flags = ((RV_DENSE if dense else 0) | (0 if graph else RV_NO_GRAPH) | (RV_PROFILE if profile else 0)
                  | (0 if attn_tc else RV_ATTN_SYNC)
-                 | (RV_WAVE_FRAME if per_frame_waves else 0))
+                 | (RV_WAVE_FRAME if per_frame_waves else 0) | (RV_CHAIN if chain else 0))
         if force_masks is not None:
             flags |= RV_FORCE_MASKS
         if device_path:

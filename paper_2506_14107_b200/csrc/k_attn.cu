@@ -60,7 +60,7 @@ template <int DH>
 __global__ void __launch_bounds__(128)
     attn_kernel(const bf16* __restrict__ q, const bf16* __restrict__ KV, const int* __restrict__ kvsrc,
                 bf16* __restrict__ out, const int4* __restrict__ wdesc, const int* __restrict__ qoff,
-                float* __restrict__ pclsh, int T, int D, int H, float scale_log2) {
+                float* __restrict__ pclsh, int T, int D, int H, float scale_log2, long long kv_ld, int q_cache) {
   constexpr int KS = DH + 8;     // padded row stride (bf16): conflict-free fragments / ldmatrix
   constexpr int CH = DH / 8;     // 16-byte chunks per row
   const int h = blockIdx.x, w = blockIdx.y;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128)
   int* rows_s = reinterpret_cast<int*>(Qs + QT * KS);  // [Tp] K/V source row of every key
   float* scls = reinterpret_cast<float*>(rows_s + Tp); // [Tp] raw CLS logits (q_cls . k_j)
   __shared__ float s_cls[2];                          // CLS row max / sum
-  const long long ld = 2LL * D;
+  const long long ld = kv_ld;       // K/V cache row stride: 2D ([k | v]) or 3D ([k | v | q], chain variant)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -93,7 +93,11 @@ __global__ void __launch_bounds__(128)
       const int r = idx / CH, c = idx % CH;
       const int row = qt * QT + r;
       const bool ok = row < nq;
-      cp_async16(Qs + r * KS + c * 8, q + (long long)(q0 + (ok ? row : 0)) * D + h * DH + c * 8, ok);
+      // q_cache (SPEC chain variant): every token of the frame is a query and its q row lives in
+      // the cache next to k and v, read through the same source-row table as the keys
+      const bf16* qsrc = q_cache ? KV + (long long)rows_s[ok ? row : 0] * ld + 2 * D + h * DH + c * 8
+                                 : q + (long long)(q0 + (ok ? row : 0)) * D + h * DH + c * 8;
+      cp_async16(Qs + r * KS + c * 8, qsrc, ok);
     }
     load_kv_block<DH>(Kr, Vr, KV, rows_s, 0, Tp, T, ld, D, h, tid);
     cp_commit();
@@ -252,7 +256,8 @@ __global__ void __launch_bounds__(128)
 
 template <int DH>
 cudaError_t launch_attn_dh(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
-                           const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s) {
+                           const int* qoff, float* pclsh, int n_w, int T, int D, int H, long long kv_ld, int q_cache,
+                           cudaStream_t s) {
   const int Tp = (T + 15) / 16 * 16;
   const size_t smem = (size_t)(4 * KB * (DH + 8) + QT * (DH + 8)) * sizeof(bf16) + (size_t)Tp * 8;
   static size_t attr = 0;
@@ -264,18 +269,20 @@ cudaError_t launch_attn_dh(const bf16* q, const bf16* KV, const int* kvsrc, bf16
   dim3 grid(H, n_w);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_kernel<DH><<<grid, 128, smem, s>>>(q, KV, kvsrc, out, reinterpret_cast<const int4*>(wdesc), qoff, pclsh, T,
-                                          D, H, scale_log2);
+                                          D, H, scale_log2, kv_ld, q_cache);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
-                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s) {
+                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s,
+                             long long kv_ld, int q_cache) {
   if (n_w <= 0) return cudaSuccess;
   const int dh = D / H;
-  if (dh == 64) return launch_attn_dh<64>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, s);
-  if (dh == 16) return launch_attn_dh<16>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, s);
+  if (kv_ld <= 0) kv_ld = 2LL * D;
+  if (dh == 64) return launch_attn_dh<64>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, kv_ld, q_cache, s);
+  if (dh == 16) return launch_attn_dh<16>(q, KV, kvsrc, out, wdesc, qoff, pclsh, n_w, T, D, H, kv_ld, q_cache, s);
   return cudaErrorInvalidValue;
 }
 

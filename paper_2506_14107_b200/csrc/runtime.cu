@@ -82,6 +82,15 @@ struct rv_ctx {
   bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *hr = nullptr;
   float* x1 = nullptr;
   unsigned long long* reuse_ctr = nullptr;   // [L]
+  // ---- SPEC chain variant (RV_CHAIN): per-layer q|k|v caches, chain inputs x'
+  int chain_cap = 0;
+  bf16* QKVc[2] = {nullptr, nullptr};  // [n][T][3D] rows [k | v | q] of layers l (even / odd)
+  float* XP = nullptr;                 // [n][T][D] chain input x'_l = X_{l-1} + Attn.Wo + bo
+  int* kvsrc2 = nullptr;               // second source-row table (layer l+1's, built by layer l)
+  float* pcl2 = nullptr;               // second CLS-attention buffer (t of the next decision)
+  int* wrows = nullptr;                // [n][T] global row f*T+i of every wave-local token, desc order
+  int* qoffT = nullptr;                // [n+1] w*T (all T tokens of a frame are queries)
+  std::vector<int> wrows_host, iota_host, qoffT_host;
   // GEMM plans (tensor maps) bound to the buffers above
   GemmPlan pe;
   CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
@@ -257,6 +266,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   if (n <= ctx->n_cap && capC <= ctx->capC && capR <= ctx->capR && max_w <= ctx->wdesc_cap) return RV_OK;
   if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
   free_list(ctx->ballocs);
+  ctx->chain_cap = 0;   // the chain-variant buffers were in the same list
   n = std::max(n, ctx->n_cap);
   capC = std::max(capC, ctx->capC);
   capR = std::max(capR, ctx->capR);
@@ -503,6 +513,195 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
 }
 
+// SPEC chain variant (RV_CHAIN; oracle/chain_ref.py):
+// per layer l, attention and W_o run densely over all T tokens; the decision taken on the chain
+// input x'_l gates FFN_l -> QKV_{l+1}; reused tokens take the provider's restored block output
+// (X_l) and its q, k, v of layer l+1 (read in place through the source-row table).  Same kernels
+// as the D1 path: the mma.sync attention in its cache-resident-q mode, the tcgen05 GEMMs with
+// row-mapped epilogues, the score / compaction / restoration kernels unchanged.
+void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patches, const float* codec,
+                        float* emb, uint8_t* masks, float* scores) {
+  const int L = ctx->L, D = ctx->D, T = ctx->T, N = ctx->N, H = ctx->H, F = ctx->F, Hr = ctx->Hr;
+  cudaStream_t s = r.s;
+  const bool dense = flags & RV_DENSE;
+  const bool force = flags & RV_FORCE_MASKS;
+  const long long ld3 = 3LL * D;
+  r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
+  --r.launches;
+  r.begin(K_PATCH,-1,-1);
+  r.chk(launch_patch_to_bf16(patches, ctx->patches_bf16, (long long)n * N, ctx->pp, ctx->KP, s), "patch_to_bf16");
+  {
+    Epi e;
+    e.out = ctx->X[0];
+    e.out_ld = D;
+    e.row_div = N;
+    e.row_add = 1;
+    r.begin(K_PE,-1,-1);
+    r.chk(gemm_launch(ctx->pe, nullptr, n * N, n * N, e, s), "gemm_pe");
+  }
+  // embed_finish also writes the uniform t of the first decision into ctx->pclsh (= P[1])
+  r.begin(K_EMBED,-1,-1);
+  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
+        "embed_finish");
+  float* P[2] = {ctx->pcl2, ctx->pclsh};       // attention of layer l writes P[l & 1]
+  int* KS[2] = {ctx->kvsrc, ctx->kvsrc2};      // source rows of layer l's q|k|v: KS[l & 1]
+  // layer-0 chain (not gated): QKV_1 of every token, per wave, into QKVc[0]
+  for (int wi = 0; wi < (int)ctx->waves.size(); ++wi) {
+    const Wave& wv = ctx->waves[wi];
+    const int rows = wv.n_w * T;
+    const int* wr = ctx->wrows + (size_t)wv.off * T;
+    r.begin(K_GATHER,0,wi);
+    r.chk(launch_gather_ln(ctx->X[0], wr, nullptr, rows, rows, ctx->lw[0].ln1_g, ctx->lw[0].ln1_b, ctx->A, D, s),
+          "gather_ln1");
+    Epi e;
+    e.bias = ctx->lw[0].bqkv;
+    e.out = ctx->QKVc[0] + 2 * D;   // q columns -> cache columns [2D, 3D)
+    e.out_rows = wr;
+    e.out_ld = ld3;
+    e.out_bf16 = 1;
+    e.split = D;
+    e.out2 = ctx->QKVc[0];          // k | v -> cache columns [0, 2D)
+    e.out2_rows = wr;
+    e.out2_ld = ld3;
+    e.out2_bf16 = 1;
+    r.begin(K_QKV,0,wi);
+    r.chk(gemm_launch(ctx->g_qkv[0], nullptr, rows, rows, e, s), "gemm_qkv");
+  }
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = ctx->lw[l];
+    float* Xin = ctx->X[l & 1];
+    float* Xout = ctx->X[(l + 1) & 1];
+    bf16* Qc = ctx->QKVc[l & 1];
+    bf16* Qn = ctx->QKVc[(l + 1) & 1];
+    for (int wi = 0; wi < (int)ctx->waves.size(); ++wi) {
+      const Wave& wv = ctx->waves[wi];
+      const int n_w = wv.n_w;
+      const int rows = n_w * T;
+      const int* wd = ctx->wdesc + (size_t)wv.off * 4;
+      const int* wr = ctx->wrows + (size_t)wv.off * T;
+      const int maxC = rows;
+      // dense attention of every token over all keys of its frame
+      r.begin(K_ATTN,l,wi);
+      r.chk(launch_attention(nullptr, Qc, KS[l & 1], ctx->att, wd, ctx->qoffT, (!dense && l + 1 < L) ? P[l & 1] : nullptr,
+                             n_w, T, D, H, s, ld3, 1),
+            "attention");
+      // W_o + residual for every token: x'_l (the chain input) into the XP cache
+      {
+        Epi e;
+        e.bias = w.bo;
+        e.resid = Xin;
+        e.resid_rows = wr;
+        e.resid_ld = D;
+        e.out = ctx->XP;
+        e.out_rows = wr;
+        e.out_ld = D;
+        r.begin(K_WO,l,wi);
+        r.chk(gemm_launch(ctx->g_wo[l], nullptr, rows, rows, e, s), "gemm_wo");
+      }
+      // decision on x' (Eq. 1-4), t = the previous layer's CLS attention
+      r.begin(K_SCORE,l,wi);
+      r.chk(launch_score(ctx->XP, T, D, N, L, l, n_w, wd, P[(l + 1) & 1], H, codec, force ? masks : nullptr,
+                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
+                         ctx->wprov, ctx->cntR, ctx->dfull, s),
+            "score");
+      // filtration; the source-row table written here serves layer l+1's q|k|v
+      r.begin(K_COMPACT,l,wi);
+      r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
+                           ctx->qoff, ctx->counts, KS[(l + 1) & 1], ctx->reuse_ctr + l,
+                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s),
+            "compact");
+      const int* MC = ctx->counts;
+      // chain FFN_l on C: LN2(x') -> FC1 -> FC2 + x', scattered to X_l rows
+      r.begin(K_LN2,l,wi);
+      r.chk(launch_gather_ln(ctx->XP, ctx->idxC, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
+      {
+        Epi e;
+        e.bias = w.b1;
+        e.act = 1;
+        e.out = ctx->h;
+        e.out_ld = F;
+        e.out_bf16 = 1;
+        r.begin(K_FC1,l,wi);
+        r.chk(gemm_launch(ctx->g_fc1[l], MC, 0, maxC, e, s), "gemm_fc1");
+      }
+      {
+        Epi e;
+        e.bias = w.b2;
+        e.resid = ctx->XP;
+        e.resid_rows = ctx->idxC;
+        e.resid_ld = D;
+        e.out = Xout;
+        e.out_rows = ctx->idxC;
+        e.out_ld = D;
+        r.begin(K_FC2,l,wi);
+        r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
+      }
+      // restoration of the block output (Delta of the chain inputs, written by the score pass)
+      if (wv.any_ref && !dense) {
+        Epi e1;
+        e1.bias = w.br1;
+        e1.act = 1;
+        e1.out = ctx->hr;
+        e1.out_ld = Hr;
+        e1.out_bf16 = 1;
+        e1.out_rows = ctx->rpos;
+        r.begin(K_R1,l,wi);
+        r.chk(gemm_launch(ctx->g_r1[l], nullptr, rows, rows, e1, s), "gemm_r1");
+        Epi e2;
+        e2.bias = w.br2;
+        e2.resid = Xout;
+        e2.resid_rows = ctx->provrow;
+        e2.resid_ld = D;
+        e2.out = Xout;
+        e2.out_rows = ctx->idxR;
+        e2.out_ld = D;
+        r.begin(K_R2,l,wi);
+        r.chk(gemm_launch(ctx->g_r2[l], ctx->counts + 1, 0, n_w * N, e2, s), "gemm_r2");
+      }
+      // chain QKV_{l+1} on C (LN1 of layer l+1), scattered into the next q|k|v cache
+      if (l + 1 < L) {
+        const LayerW& wn = ctx->lw[l + 1];
+        r.begin(K_GATHER,l + 1,wi);
+        r.chk(launch_gather_ln(Xout, ctx->idxC, MC, 0, maxC, wn.ln1_g, wn.ln1_b, ctx->A, D, s), "gather_ln1");
+        Epi e;
+        e.bias = wn.bqkv;
+        e.out = Qn + 2 * D;
+        e.out_rows = ctx->idxC;
+        e.out_ld = ld3;
+        e.out_bf16 = 1;
+        e.split = D;
+        e.out2 = Qn;
+        e.out2_rows = ctx->idxC;
+        e.out2_ld = ld3;
+        e.out2_bf16 = 1;
+        r.begin(K_QKV,l + 1,wi);
+        r.chk(gemm_launch(ctx->g_qkv[l + 1], MC, 0, maxC, e, s), "gemm_qkv");
+      }
+    }
+  }
+  r.begin(K_LNPOST,-1,-1);
+  r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
+}
+
+rv_status ensure_chain_buffers(rv_ctx* ctx, int n) {
+  if (n <= ctx->chain_cap) return RV_OK;
+  const long long T = ctx->T, D = ctx->D;
+  auto& B = ctx->ballocs;
+  rv_status s;
+#define AL(ptr, cnt) if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) return s
+  AL(ctx->QKVc[0], n * T * 3 * D);
+  AL(ctx->QKVc[1], n * T * 3 * D);
+  AL(ctx->XP, n * T * D);
+  AL(ctx->kvsrc2, n * T);
+  AL(ctx->pcl2, (long long)n * ctx->H * ctx->N);
+  AL(ctx->wrows, n * T);
+  AL(ctx->qoffT, n + 1);
+#undef AL
+  ctx->chain_cap = n;
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  return RV_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -743,6 +942,17 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   if (total_desc != n) return fail(ctx, RV_EPLAN, "rv_embed: internal wave bookkeeping mismatch");
   if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w)))
     return st;
+  if (flags & RV_CHAIN) {
+    if ((st = ensure_chain_buffers(ctx, n))) return st;
+    const int nd = (int)ctx->wdesc_host.size() / 4;
+    ctx->wrows_host.resize((size_t)nd * T);
+    for (int k = 0; k < nd; ++k)
+      for (int i = 0; i < T; ++i) ctx->wrows_host[(size_t)k * T + i] = ctx->wdesc_host[(size_t)k * 4] * T + i;
+    ctx->iota_host.resize((size_t)n * T);
+    for (size_t i = 0; i < ctx->iota_host.size(); ++i) ctx->iota_host[i] = (int)i;
+    ctx->qoffT_host.resize((size_t)n + 1);
+    for (int w = 0; w <= n; ++w) ctx->qoffT_host[w] = w * T;
+  }
   {
     const int need = L * (int)ctx->waves.size() * 2;
     if (need > ctx->count_log_cap) {
@@ -771,6 +981,14 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   CK(cudaEventRecord(ctx->ev[0], ws));
   CK(cudaMemcpyAsync(ctx->wdesc, ctx->wdesc_host.data(), ctx->wdesc_host.size() * sizeof(int),
                      cudaMemcpyHostToDevice, ws));
+  if (flags & RV_CHAIN) {   // wave row map, query offsets, identity source rows of layer 1's q|k|v
+    CK(cudaMemcpyAsync(ctx->wrows, ctx->wrows_host.data(), ctx->wrows_host.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ws));
+    CK(cudaMemcpyAsync(ctx->qoffT, ctx->qoffT_host.data(), ctx->qoffT_host.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ws));
+    CK(cudaMemcpyAsync(ctx->kvsrc, ctx->iota_host.data(), ctx->iota_host.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ws));
+  }
   if (!devp) {
     CK(cudaMemcpyAsync(ctx->in_patches, patches, (size_t)n * N * ctx->pp * 4, cudaMemcpyHostToDevice, ws));
     CK(cudaMemcpyAsync(ctx->in_codec, codec, (size_t)n * N * 4, cudaMemcpyHostToDevice, ws));
@@ -789,7 +1007,8 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   if (flags & RV_NO_GRAPH) {
     ctx->prof_used = 0;
     ctx->prof_recs.clear();
-    record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
+    (flags & RV_CHAIN ? record_embed_chain : record_embed)(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks,
+                                                          d_scores);
     if (rec.err != cudaSuccess) return fail(ctx, RV_ECUDA, "launch %s: %s", rec.where, cudaGetErrorString(rec.err));
   } else {
     if (!ctx->gexec || key != ctx->gkey) {
@@ -798,7 +1017,8 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
       ctx->prof_used = 0;
       ctx->prof_recs.clear();
       CK(cudaStreamBeginCapture(ws, cudaStreamCaptureModeThreadLocal));
-      record_embed(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks, d_scores);
+      (flags & RV_CHAIN ? record_embed_chain : record_embed)(ctx, rec, n, flags, d_patches, d_codec, d_emb, d_masks,
+                                                          d_scores);
       cudaError_t ce = cudaStreamEndCapture(ws, &g);
       if (rec.err != cudaSuccess) {
         if (g) cudaGraphDestroy(g);
@@ -849,12 +1069,17 @@ rv_status rv_wait(rv_ctx* ctx, rv_stats* stats) {
   const double D = ctx->D, F = ctx->F, Hr = ctx->Hr, pp = ctx->pp;
   const double per_c = 2 * D * 3 * D + 2 * D * D + 4 * D * F + 4 * T * D;
   const double per_r = 4 * D * Hr;
+  const bool chain = ctx->cur_flags & RV_CHAIN;
   double reused = 0, flops = 2.0 * n * N * pp * D, bytes = 0;
+  if (chain) flops += (double)n * T * 2 * D * 3 * D;   // QKV_1 of every token (ungated layer-0 chain)
   for (int l = 0; l < L; ++l) {
     const double r = (double)ctr[l];
     const double c = (double)n * T - r;
     reused += r;
-    flops += c * per_c + r * per_r;
+    if (chain)   // attention + W_o dense; FFN_l (+ QKV_{l+1}) on C; restoration on R
+      flops += (double)n * T * (4 * T * D + 2 * D * D) + c * (4 * D * F + (l + 1 < L ? 6 * D * D : 0.0)) + r * per_r;
+    else
+      flops += c * per_c + r * per_r;
     // algorithmic bytes: 60 D per recomputed token-layer, 18 D per reused one
     bytes += c * 60.0 * D + r * 18.0 * D;
     stats->reuse_by_layer[l] = ctx->cur_nonI ? (float)(r / ((double)ctx->cur_nonI * N)) : 0.f;

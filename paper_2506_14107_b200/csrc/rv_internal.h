@@ -77,6 +77,9 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV,
                                 bf16* out,
                                 const int* wdesc, const int* qoff, float* pclsh, int n_w, int T, int D, int H,
                                 cudaStream_t s);
+// kv_ld: K/V cache row stride (0 -> 2D); q_cache: queries are all T tokens of each frame with q read
+// from the cache row at column 2D through kvsrc (SPEC chain variant), qoff[w] = w*T
 cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
-                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s);
+                             const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s,
+                             long long kv_ld = 0, int q_cache = 0);
 }  // namespace rv

@@ -145,6 +145,31 @@ def test_determinism_graph_and_host_paths(cuda_ok):
     assert st["ms_total"] > 0 and st["n_launches"] > 0
 
 
+@pytest.mark.parametrize("cfgname,n,n_check,p", [("tiny", 12, 12, 0.3), ("b16", 24, 24, 0.3), ("l14", 32, 9, 0.2)])
+def test_chain_variant_parity(cuda_ok, cfgname, n, n_check, p):
+    """SURVEY §8(f) NEXT-1, SPEC chain variant (RV_CHAIN: decision on the FFN input gates
+    FFN_l -> QKV_{l+1}, attention + W_o dense) vs oracle.reuse_embed_chain."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, n, p, seed=3000 + n)
+    plan = oracle.plan_gop(n)
+    Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), chain=True, want_scores=True)
+    torch.cuda.synchronize()
+    frames = list(range(n_check))
+    ref = oracle.reuse_embed_chain(cfg, W, G, x, c, plan, frames=frames)
+    err, cos = metrics(Z.cpu().numpy()[frames], ref["Z"][frames])
+    agree, cnt = mask_agreement(M.cpu().numpy(), ref, frames)
+    print(f"chain {cfgname} n={n}: reuse_all={st['reuse_all']:.3f} max_err={err.max():.3e} "
+          f"min_cos={cos.min():.6f} mask_agree={agree:.5f} ({cnt} tokens)")
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and agree >= 0.999
+    assert st["reuse_all"] > 0.2
+    # the same frames with the chain variant forced dense equal the plain ViT
+    Zd, Md, _, std_ = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), chain=True, dense=True)
+    torch.cuda.synchronize()
+    err, cos = metrics(Zd.cpu().numpy()[frames], oracle.dense_embed(cfg, W, x[:n_check]))
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and std_["reuse_all"] == 0.0
+
+
 @pytest.mark.parametrize("cfgname,n,n_check", [("tiny", 25, 25), ("b16", 24, 24)])
 def test_streaming_mode_parity(cuda_ok, cfgname, n, n_check):
     """SURVEY §8(f) NEXT-3, low-latency mode: reordering off, every frame is a P
