@@ -44,7 +44,7 @@ def classify(names):
             ln += 1
         elif "rgather" in n or "gather_rows" in n:
             out.append("rgather")
-        elif "attn_kernel" in n:
+        elif "attn" in n:
             out.append("attention")
         elif "gemm_tc_kernel" in n:
             if gi is None:
