@@ -291,6 +291,10 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     prof = m.profile()                 # per-class event timings of the last timed step
+    wc = m.wave_counts()               # level-wave sizes and recomputed / reused rows
+    waves_info = {"frames_per_wave": wc["frames"].tolist(),
+                  "M_C_mean_over_layers": [round(float(v), 1) for v in wc["M_C"].mean(axis=0)],
+                  "M_R_mean_over_layers": [round(float(v), 1) for v in wc["M_R"].mean(axis=0)]}
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -419,6 +423,7 @@ def main():
                        "compute": "bf16 operands, fp32 accumulate, fp32 residual",
                        "variant": "SPEC chain (RV_CHAIN)" if args.chain else "D1 layer-gated (default)"},
             "reuse": {"reuse_all": stats["reuse_all"], "reuse_nonI": stats["reuse_nonI"]},
+            "waves": waves_info,
             "flops_exec_per_step": stats["flops_exec"], "flops_dense_per_step": stats["flops_dense"],
             "tc_frac_exec": stats["flops_exec"] / (ms / 1e3) / 1e12 / peaks["tc_sustained"],
             "gemm": {"ms_per_step": gemm_ms, "tflops": gemm_fl / max(gemm_ms, 1e-9) / 1e9,

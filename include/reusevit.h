@@ -168,6 +168,14 @@ rv_status rv_wait(rv_ctx* ctx, rv_stats* stats);
  * written, or a negative rv_status.  Event durations are taken on the embed's stream. */
 int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries);
 
+/* After rv_wait: the level-wave structure of the last embed ("report the
+ * level-size histogram and per-level M_C").  frames [max_waves] receives the frames of every
+ * wave (waves in execution order: dependency levels, large levels split); counts
+ * [L][n_waves][2] receives (M_C recomputed rows incl. CLS, M_R reused rows) per layer and wave.
+ * Returns the number of waves (also when max_waves is too small or the buffers are NULL: a size
+ * query), or a negative rv_status. */
+int32_t rv_wave_counts(rv_ctx* ctx, int32_t* frames, int32_t* counts, int32_t max_waves);
+
 /* Human-readable message for the last error on ctx (never NULL; "" when none).  With
  * ctx == NULL returns the last rv_create failure message. */
 const char* rv_last_error(const rv_ctx* ctx);

@@ -70,6 +70,7 @@ SIGNATURES = {
     "rv_stage_compact": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rv_stage_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "rv_stage_attention": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "rv_wave_counts": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
     "rv_f32_to_f16": (c_i32, [c_vp, c_vp, ctypes.c_int64, c_vp]),
     "rv_topk_cosine": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
 }

@@ -177,6 +177,20 @@ class ReuseViT:
                 "ms_total": s.ms_total, "ms_compute": s.ms_compute, "n_levels": s.n_levels,
                 "n_launches": s.n_launches, "reuse_by_layer": list(s.reuse_by_layer[:L])}
 
+    def wave_counts(self) -> dict:
+        """Level-wave structure of the last embed (after ``wait``): frames per wave and the
+        per-layer recomputed / reused row counts."""
+        k = self.lib.rv_wave_counts(self.h, None, None, 0)
+        if k < 0:
+            check(self.lib, k, self.h)
+        frames = np.zeros(k, np.int32)
+        counts = np.zeros((self.cfg.layers, k, 2), np.int32)
+        check_k = self.lib.rv_wave_counts(self.h, frames.ctypes.data_as(ctypes.c_void_p),
+                                          counts.ctypes.data_as(ctypes.c_void_p), k)
+        if check_k < 0:
+            check(self.lib, check_k, self.h)
+        return {"frames": frames, "M_C": counts[:, :, 0], "M_R": counts[:, :, 1]}
+
     def profile(self) -> list:
         """Per-kernel-class records of the last ``profile=True`` embed (after ``wait``)."""
         buf = (RvKernelProf * 32)()

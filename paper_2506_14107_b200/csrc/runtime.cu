@@ -1116,6 +1116,18 @@ void rv_destroy(rv_ctx* ctx) {
   delete ctx;
 }
 
+int32_t rv_wave_counts(rv_ctx* ctx, int32_t* frames, int32_t* counts, int32_t max_waves) {
+  if (!ctx) return RV_ECONTRACT;
+  if (ctx->inflight || ctx->waves.empty())
+    return fail(ctx, RV_ECONTRACT, "rv_wave_counts: no completed embed (call rv_wait first)");
+  const int nwv = (int)ctx->waves.size();
+  if (!frames || !counts || max_waves < nwv) return nwv;   // size query
+  CK(cudaSetDevice(ctx->device));
+  for (int wi = 0; wi < nwv; ++wi) frames[wi] = ctx->waves[wi].n_w;
+  CK(cudaMemcpy(counts, ctx->count_log, (size_t)ctx->L * nwv * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  return nwv;
+}
+
 int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
   if (!ctx || !out) return RV_ECONTRACT;
   if (!ctx->prof_valid || ctx->inflight)
