@@ -209,6 +209,9 @@ def run_reference(args):
                              "sample": f"display frames 0-{sample - 1} of the {args.frames}-frame video"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(json.dumps(line) + "\n")
 
 
 def main():
