@@ -51,6 +51,16 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
                         const void* B, const float* bias, int32_t act, void* out,
                         int32_t out_bf16, void* stream);
 
+/* a9 / a11 / a12 building block — the same GEMM with the row-mapped epilogue of the embed:
+ * out[out_rows[m]][n] = act(A[m] . B[n] + bias[n]) + resid[resid_rows[m]][n]  (fp32 resid,
+ * NULL = none; resid_rows / out_rows NULL = identity; an out_rows entry < 0 skips row m).
+ * K <= 128 with a residual selects the short-K residual-streaming variant (restoration R2,
+ * Eq. 9-10).  Leading dimensions in elements.  RV_ECONTRACT on bad arguments. */
+rv_status rv_stage_gemm_rows(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void* A,
+                             const void* B, const float* bias, int32_t act, const float* resid,
+                             const int32_t* resid_rows, int64_t resid_ld, void* out,
+                             const int32_t* out_rows, int64_t out_ld, int32_t out_bf16, void* stream);
+
 /* a8 — attention of compacted queries over all T keys of their frame:
  * q [M_C][D] bf16 (rows qoff[w]..qoff[w+1]-1 belong to wave frame w, first row = CLS),
  * KV [slots][T][2D] bf16 (K in columns 0..D-1, V in D..2D-1, head h = columns h*dh..),

@@ -69,6 +69,8 @@ SIGNATURES = {
     "rv_stage_score": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rv_stage_compact": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rv_stage_gemm": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
+    "rv_stage_gemm_rows": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, ctypes.c_int64,
+                                   c_vp, c_vp, ctypes.c_int64, c_i32, c_vp]),
     "rv_stage_attention": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "rv_wave_counts": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
     "rv_f32_to_f16": (c_i32, [c_vp, c_vp, ctypes.c_int64, c_vp]),

@@ -228,6 +228,19 @@ class ReuseViT:
                                                1 if out_bf16 else 0, ctypes.c_void_p(stream.cuda_stream)), self.h)
         return out
 
+    def stage_gemm_rows(self, A, B, out, bias=None, act=0, resid=None, resid_rows=None, out_rows=None,
+                        stream=None):
+        """out[out_rows[m]] = act(A[m] B^T + bias) + resid[resid_rows[m]] (row-mapped epilogue)."""
+        import torch
+        M, K = A.shape
+        N = B.shape[0]
+        stream = stream or torch.cuda.current_stream(A.device)
+        check(self.lib, self.lib.rv_stage_gemm_rows(
+            self.h, M, N, K, _ptr(A), _ptr(B), _ptr(bias), act, _ptr(resid), _ptr(resid_rows),
+            resid.shape[1] if resid is not None else 0, _ptr(out), _ptr(out_rows), out.shape[1],
+            1 if out.dtype == torch.bfloat16 else 0, ctypes.c_void_p(stream.cuda_stream)), self.h)
+        return out
+
     def stage_attention(self, wdesc, qoff, q, KV, out, pcls, stream, use_tc=False, kvsrc=None):
         check(self.lib, self.lib.rv_stage_attention(self.h, wdesc.shape[0], _ptr(wdesc), _ptr(qoff), _ptr(q),
                                                     q.shape[0], _ptr(KV), _ptr(kvsrc), _ptr(out), _ptr(pcls),

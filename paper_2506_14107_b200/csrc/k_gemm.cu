@@ -32,11 +32,12 @@ constexpr int BK = 64;            // 64 bf16 = 128 B = one SWIZZLE_128B atom row
 constexpr int GEMM_THREADS = 320;   // TMA warp + MMA/TMEM warp + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 
-constexpr int RDEPTH = 3;         // residual chunks in flight per epilogue warp (SR variant)
+constexpr int RDEPTH = 4;         // residual chunks in flight per epilogue warp (SR variant)
 
 // SR ("short K, streaming residual"): for K <= 256 the mainloop needs only 2 stages, and the
-// freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep, so the
-// HBM-bound epilogue keeps ~96 KB of residual loads in flight per SM.
+// freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep; the chunk's
+// ring slot doubles as its transpose tile once the residual is in registers, so the HBM-bound
+// epilogue keeps 128 KB of residual loads in flight per SM.
 template <int BN, bool SR>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -44,7 +45,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = SR ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int STAGE_OUT = EPI_WARPS * (32 * 32 + 64) * 4;   // per-warp 32x32 fp32 transpose tile + row maps
+  // per-warp 32x32 fp32 transpose tile + row maps (SR: row maps only; the ring slot is the tile)
+  static constexpr int STAGE_OUT = SR ? EPI_WARPS * 64 * 4 : EPI_WARPS * (32 * 32 + 64) * 4;
   static constexpr int RESID = SR ? EPI_WARPS * RDEPTH * 32 * 32 * 4 : 0;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT + RESID + 256 /*barriers*/;
   static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
@@ -241,10 +243,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // loaded once per tile and the 8 residual loads of a chunk are issued together (MLP).
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
-    float* tile_s = sOut + (warp - 2) * (32 * 32 + 64);
-    int* orow_s = reinterpret_cast<int*>(tile_s + 32 * 32);   // [32] output row of each tile row
-    int* rrow_s = orow_s + 32;                                  // [32] residual row
-    const uint32_t tile_u = smem_u32(tile_s);
+    float* tile_s = SR ? nullptr : sOut + (warp - 2) * (32 * 32 + 64);
+    int* orow_s = SR ? reinterpret_cast<int*>(sOut) + (warp - 2) * 64
+                     : reinterpret_cast<int*>(tile_s + 32 * 32);   // [32] output row of each tile row
+    int* rrow_s = orow_s + 32;                                       // [32] residual row
+    uint32_t tile_u = SR ? 0u : smem_u32(tile_s);
     const int rsub = lane >> 3;          // row within a group of 4
     const int c4 = (lane & 7) * 4;       // first of this lane's 4 columns
     int it = 0;
@@ -314,6 +317,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               xc[i] = lds128(ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4));
             }
           }
+          // the slot's residual is in registers: it now serves as this chunk's transpose tile
+          tile_u = ring + (uint32_t)((c % RDEPTH) * 32 * 128);
+          __syncwarp();
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) xc[i] = xn[i];
@@ -357,10 +363,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off) = v;
           }
         }
+        __syncwarp();   // every lane has read the (transpose tile in the) slot
         if constexpr (SR) {
           if (e.resid) issue_resid(c + RDEPTH);   // refill the slot consumed above
         }
-        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);

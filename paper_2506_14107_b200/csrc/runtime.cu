@@ -1230,6 +1230,31 @@ rv_status rv_stage_gemm(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void
   return RV_OK;
 }
 
+rv_status rv_stage_gemm_rows(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const void* A, const void* B,
+                             const float* bias, int32_t act, const float* resid, const int32_t* resid_rows,
+                             int64_t resid_ld, void* out, const int32_t* out_rows, int64_t out_ld, int32_t out_bf16,
+                             void* stream) {
+  if (!ctx) return RV_ECONTRACT;
+  if (M < 0 || N % 64 || K % 64 || N <= 0 || K <= 0 || !A || !B || !out || out_ld < N || (resid && resid_ld < N))
+    return fail(ctx, RV_ECONTRACT, "rv_stage_gemm_rows: bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  GemmPlan p;
+  char e[256];
+  if (!gemm_make_plan(&p, A, std::max(M, 1), B, N, K, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+  Epi ep;
+  ep.bias = bias;
+  ep.act = act;
+  ep.resid = resid;
+  ep.resid_rows = resid_rows;
+  ep.resid_ld = resid_ld;
+  ep.out = out;
+  ep.out_rows = out_rows;
+  ep.out_ld = out_ld;
+  ep.out_bf16 = out_bf16;
+  CK(gemm_launch(p, nullptr, M, M, ep, (cudaStream_t)stream));
+  return RV_OK;
+}
+
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const int32_t* qoff, const void* q,
                              int32_t q_rows, const void* KV, const int32_t* kvsrc, void* out, float* pcls,
                              int32_t use_tc, void* stream) {

@@ -70,6 +70,37 @@ def test_gemm_row_position_invariance(dev):
     assert torch.equal(full[300:700], shifted)
 
 
+@pytest.mark.parametrize("M,N,K,act", [(700, 1024, 128, 0), (5000, 768, 128, 0), (1000, 1024, 1024, 0),
+                                       (300, 4096, 1024, 1)])
+def test_gemm_row_mapped_epilogue_vs_torch(dev, M, N, K, act):
+    """Row-mapped epilogue (W_o / FC2 / restoration R2, Eq. 9-10): gathered fp32 residual rows,
+    scattered output rows (entries < 0 skipped); K = 128 takes the short-K streaming variant."""
+    cfg = synth.CONFIGS["b16"]
+    m, _, _ = _model(cfg, gates=False)
+    g = torch.Generator(device=dev).manual_seed(M + N)
+    A = (0.5 * torch.randn(M, K, device=dev, generator=g)).to(torch.bfloat16)
+    B = (0.05 * torch.randn(N, K, device=dev, generator=g)).to(torch.bfloat16)
+    bias = torch.randn(N, device=dev, generator=g)
+    rows = 3 * M
+    resid = torch.randn(rows, N, device=dev, generator=g)
+    rrows = torch.randperm(rows, device=dev, generator=g)[:M].to(torch.int32)
+    orows = torch.randperm(rows, device=dev, generator=g)[:M].to(torch.int32)
+    orows[::7] = -1
+    out = torch.full((rows, N), 7.0, device=dev)
+    m.stage_gemm_rows(A, B, out, bias=bias, act=act, resid=resid, resid_rows=rrows, out_rows=orows)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T + bias
+    if act:
+        ref = ref * torch.sigmoid(1.702 * ref)
+    ref = ref + resid[rrows.long()]
+    keep = orows >= 0
+    got = out[orows[keep].long()]
+    assert (got - ref[keep]).abs().max().item() < 2e-2 * (1 + ref.abs().max().item() * 1e-2)
+    untouched = torch.ones(rows, dtype=torch.bool, device=dev)
+    untouched[orows[keep].long()] = False
+    assert torch.all(out[untouched] == 7.0)
+
+
 # ------------------------------------------------------------------------- attention
 @pytest.mark.parametrize("cfgname,use_tc", [("tiny", False), ("b16", False), ("l14", False), ("l14_336", False),
                                             ("b16", True), ("l14", True)])
