@@ -11,7 +11,7 @@
 //   warp 0 : TMA producer (one elected lane), STAGES-deep smem ring, SWIZZLE_128B tiles
 //   warp 1 : MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
 //   warp 1 also allocates TMEM (2*BN fp32 columns: double-buffered accumulator)
-//   warps 2-9 : epilogue (warp%4 = TMEM lane quarter, (warp-2)/4 = column half):
+//   warps 2.. : epilogue, 8 (16 in the SR variant) (warp%4 = TMEM lane quarter, (warp-2)/4 = column slice):
 //               tcgen05.ld 32x32b.x32 -> smem transpose -> coalesced bias / QuickGELU /
 //               residual / row-mapped (scatter) stores in fp32 or bf16
 // Fixed tiles and no split-K: every output element is accumulated in the same K order
@@ -29,10 +29,13 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;            // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int GEMM_THREADS = 320;   // TMA warp + MMA/TMEM warp + 8 epilogue warps
-constexpr int EPI_WARPS = 8;
+// TMA warp + MMA/TMEM warp + epilogue warps: 8, or 16 for the short-K residual-streaming (SR)
+// variant, whose epilogue is a chain of dependent latencies per chunk and needs more warps
+// (at least one 32-column chunk per warp: 16 warps need BN >= 128)
+template <int BN, bool SR> constexpr int epi_warps() { return SR && BN >= 128 ? 16 : 8; }
+template <int BN, bool SR> constexpr int gemm_threads() { return (2 + epi_warps<BN, SR>()) * 32; }
 
-constexpr int RDEPTH = 4;         // residual chunks in flight per epilogue warp (SR variant)
+constexpr int RDEPTH = 2;         // residual chunks in flight per epilogue warp (SR variant)
 
 // SR ("short K, streaming residual"): for K <= 256 the mainloop needs only 2 stages, and the
 // freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep; the chunk's
@@ -45,9 +48,11 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = SR ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  // per-warp 32x32 fp32 transpose tile + row maps (SR: row maps only; the ring slot is the tile)
-  static constexpr int STAGE_OUT = SR ? EPI_WARPS * 64 * 4 : EPI_WARPS * (32 * 32 + 64) * 4;
-  static constexpr int RESID = SR ? EPI_WARPS * RDEPTH * 32 * 32 * 4 : 0;
+  static constexpr int EPI = epi_warps<BN, SR>();
+  // per-warp 32x32 fp32 transpose tile + row maps (SR: output rows only; the ring slot is the
+  // tile and the residual rows travel by shuffle)
+  static constexpr int STAGE_OUT = SR ? EPI * 32 * 4 : EPI * (32 * 32 + 64) * 4;
+  static constexpr int RESID = SR ? EPI * RDEPTH * 32 * 32 * 4 : 0;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT + RESID + 256 /*barriers*/;
   static_assert(SMEM <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
@@ -149,7 +154,7 @@ RV_DEV float quick_gelu_fast(float x) {
 }
 
 template <int BN, bool SR>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(gemm_threads<BN, SR>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
   using C = Cfg<BN, SR>;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS * 32);
+      mbar_init(&tempty[a], C::EPI * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -242,11 +247,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // access) -> bias / QuickGELU / residual / row-mapped store, all coalesced.  Row maps are
     // loaded once per tile and the 8 residual loads of a chunk are issued together (MLP).
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;    // column slice of this warp (of C::EPI / 4)
     float* tile_s = SR ? nullptr : sOut + (warp - 2) * (32 * 32 + 64);
-    int* orow_s = SR ? reinterpret_cast<int*>(sOut) + (warp - 2) * 64
+    int* orow_s = SR ? reinterpret_cast<int*>(sOut) + (warp - 2) * 32
                      : reinterpret_cast<int*>(tile_s + 32 * 32);   // [32] output row of each tile row
-    int* rrow_s = orow_s + 32;                                       // [32] residual row
+    int* rrow_s = orow_s + 32;                                       // [32] residual row (not SR)
+    int rrow_reg = 0;                                                // SR: residual row of row `lane`
     uint32_t tile_u = SR ? 0u : smem_u32(tile_s);
     const int rsub = lane >> 3;          // row within a group of 4
     const int c4 = (lane & 7) * 4;       // first of this lane's 4 columns
@@ -261,11 +267,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int m = row0 + lane;
         const int mm = m < M ? m : 0;
         orow_s[lane] = e.out_rows ? __ldg(e.out_rows + mm) : mm + (e.row_div ? mm / e.row_div : 0) + e.row_add;
-        rrow_s[lane] = e.resid ? (e.resid_rows ? __ldg(e.resid_rows + mm) : mm) : 0;
+        const int rv = e.resid ? (e.resid_rows ? __ldg(e.resid_rows + mm) : mm) : 0;
+        if constexpr (SR) rrow_reg = rv; else rrow_s[lane] = rv;
       }
       const int nvalid = min(32, M - row0);     // rows of this warp that exist (may be <= 0)
       __syncwarp();
-      const int c_beg = half * (BN / 64), c_end = (half + 1) * (BN / 64);
+      constexpr int CPW = (BN / 32) / (C::EPI / 4);   // 32-column chunks per warp and tile
+      static_assert(CPW >= 1, "every epilogue warp needs a column chunk");
+      const int c_beg = half * CPW, c_end = (half + 1) * CPW;
       // Residual rows are known before the accumulator is: load chunk c+1's residual while
       // chunk c is processed (8 x 16 B in flight per lane; the first batch overlaps the MMA).
       float4 xn[8];
@@ -287,7 +296,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int i = 0; i < 8; ++i) {
             const int rr = i * 4 + rsub;
             const bool live = rr < nvalid && orow_s[rr] >= 0;
-            const float* src = e.resid + (long long)rrow_s[live ? rr : 0] * e.resid_ld + nb * BN + c * 32 + c4;
+            const int rrow = __shfl_sync(0xffffffffu, rrow_reg, live ? rr : 0);
+            const float* src = e.resid + (long long)rrow * e.resid_ld + nb * BN + c * 32 + c4;
             const uint32_t dst = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                          "r"(live ? 16 : 0)
@@ -440,7 +450,7 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
     const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
     int grid = tiles < num_sms() ? tiles : num_sms();
     if (grid < 1) grid = 1;
-    gemm_tc_kernel<BN, true><<<grid, GEMM_THREADS, C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+    gemm_tc_kernel<BN, true><<<grid, gemm_threads<BN, true>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
     return cudaGetLastError();
   }
   using C = Cfg<BN, false>;
@@ -454,7 +464,7 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, false><<<grid, GEMM_THREADS, C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+  gemm_tc_kernel<BN, false><<<grid, gemm_threads<BN, false>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
   return cudaGetLastError();
 }
 
