@@ -32,8 +32,10 @@ constexpr int BK = 64;            // 64 bf16 = 128 B = one SWIZZLE_128B atom row
 // TMA warp + MMA/TMEM warp + epilogue warps: 8, or 16 for the short-K residual-streaming (SR)
 // variant, whose epilogue is a chain of dependent latencies per chunk and needs more warps
 // (at least one 32-column chunk per warp: 16 warps need BN >= 128)
-template <int BN, bool SR> constexpr int epi_warps() { return SR && BN >= 128 ? 16 : 8; }
-template <int BN, bool SR> constexpr int gemm_threads() { return (2 + epi_warps<BN, SR>()) * 32; }
+// MODE 0: plain; 1 (SR): short K with a streamed residual (restoration R2); 2 (RE): K <= 1024
+// with a gathered residual (W_o): 16 epilogue warps and 3 mainloop stages
+template <int BN, int MODE> constexpr int epi_warps() { return MODE != 0 && BN >= 128 ? 16 : 8; }
+template <int BN, int MODE> constexpr int gemm_threads() { return (2 + epi_warps<BN, MODE>()) * 32; }
 
 constexpr int RDEPTH = 2;         // residual chunks in flight per epilogue warp (SR variant)
 
@@ -41,14 +43,15 @@ constexpr int RDEPTH = 2;         // residual chunks in flight per epilogue warp
 // freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep; the chunk's
 // ring slot doubles as its transpose tile once the residual is in registers, so the HBM-bound
 // epilogue keeps 128 KB of residual loads in flight per SM.
-template <int BN, bool SR>
+template <int BN, int MODE>
 struct Cfg {
+  static constexpr bool SR = MODE == 1;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = SR ? 2 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  static constexpr int STAGES = SR ? 2 : MODE == 2 ? 3 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int EPI = epi_warps<BN, SR>();
+  static constexpr int EPI = epi_warps<BN, MODE>();
   // per-warp 32x32 fp32 transpose tile + row maps (SR: output rows only; the ring slot is the
   // tile and the residual rows travel by shuffle)
   static constexpr int STAGE_OUT = SR ? EPI * 32 * 4 : EPI * (32 * 32 + 64) * 4;
@@ -153,11 +156,12 @@ RV_DEV float quick_gelu_fast(float x) {
   return x * fmaf(0.5f, t, 0.5f);
 }
 
-template <int BN, bool SR>
-__global__ void __launch_bounds__(gemm_threads<BN, SR>(), 1)
+template <int BN, int MODE>
+__global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
-  using C = Cfg<BN, SR>;
+  using C = Cfg<BN, MODE>;
+  constexpr bool SR = C::SR;
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // SWIZZLE_128B needs 1024-B aligned stages
   uint8_t* smem = smem_raw;
   uint8_t* sA = smem;
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, SR>(), 1)
       if (e.resid) {
         if constexpr (SR) {
           for (int k = 0; k < RDEPTH; ++k) issue_resid(c_beg + k);
-        } else {
+        } else if constexpr (MODE == 0) {
           load_resid(c_beg, xn);
         }
       }
@@ -330,10 +334,14 @@ __global__ void __launch_bounds__(gemm_threads<BN, SR>(), 1)
           // the slot's residual is in registers: it now serves as this chunk's transpose tile
           tile_u = ring + (uint32_t)((c % RDEPTH) * 32 * 128);
           __syncwarp();
-        } else {
+        } else if constexpr (MODE == 0) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) xc[i] = xn[i];
           if (e.resid && c + 1 < c_end) load_resid(c + 1, xn);
+        } else {
+          // RE: twice the warps hide the latency; this chunk's residual loads overlap the
+          // TMEM load and the transpose below (no register prefetch: 96 registers per thread)
+          if (e.resid) load_resid(c, xc);
         }
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
@@ -434,38 +442,33 @@ int num_sms() {
   return n;
 }
 
-template <int BN>
-cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
-                      cudaStream_t s) {
-  // short K with a residual: 2-stage mainloop + cp.async residual ring (see Cfg)
-  if (p.K <= 2 * BK && e.resid) {
-    using C = Cfg<BN, true>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t err =
-          cudaFuncSetAttribute(gemm_tc_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-      if (err != cudaSuccess) return err;
-      attr = true;
-    }
-    const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
-    int grid = tiles < num_sms() ? tiles : num_sms();
-    if (grid < 1) grid = 1;
-    gemm_tc_kernel<BN, true><<<grid, gemm_threads<BN, true>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
-    return cudaGetLastError();
-  }
-  using C = Cfg<BN, false>;
+template <int BN, int MODE>
+cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
+  using C = Cfg<BN, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t err =
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           C::SMEM);
     if (err != cudaSuccess) return err;
     attr = true;
   }
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, false><<<grid, gemm_threads<BN, false>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+  gemm_tc_kernel<BN, MODE><<<grid, gemm_threads<BN, MODE>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
   return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
+                      cudaStream_t s) {
+  // short K with a residual: 2-stage mainloop + cp.async residual ring (R2); a gathered residual
+  // with K <= 1024 (W_o): 16 epilogue warps, 3 stages (tools/r2_bench.py: 57 -> 52 us on a
+  // 16k-row W_o; FC2's K = 4096 mainloop needs its 4 stages).  RV_GEMM_RE=0 disables.
+  static const bool re_on = !getenv("RV_GEMM_RE") || atoi(getenv("RV_GEMM_RE")) != 0;
+  if (p.K <= 2 * BK && e.resid) return launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
+  if (e.resid && BN >= 128 && p.K <= 1024 && re_on) return launch_mode<BN, 2>(p, M_dev, M_host, max_m, e, s);
+  return launch_mode<BN, 0>(p, M_dev, M_host, max_m, e, s);
 }
 
 }  // namespace
