@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--attn-sync", action="store_true", help="mma.sync attention kernel (RV_ATTN_SYNC) instead of tcgen05")
     ap.add_argument("--chain", action="store_true", help="SPEC chain variant (RV_CHAIN, SURVEY NEXT-1) instead of D1")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: the 7,200-frame L/14 video (default); c5: L/14@336 multi-video, LPT-sharded")
+    ap.add_argument("--videos", type=int, default=64)
+    ap.add_argument("--video-frames", type=int, default=120)
     return ap.parse_args()
 
 
@@ -214,10 +218,114 @@ def run_reference(args):
             fh.write(json.dumps(line) + "\n")
 
 
+def run_c5(args):
+    """BASELINE configs[4] / SURVEY C5: ViT-L/14 336 px (T = 577) ReuseViT, 64 videos x 120
+    frames (60-s clips at 2 FPS) with heterogeneous motion p in {.05, .1, .2, .4}; videos
+    are assigned to the ranks by LPT on their estimated cost sum(1 - r_hat) and
+    each rank embeds its videos in ONE call (combined block-diagonal plan), then the
+    embeddings are all-gathered.  One step = embed + gather; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2506_14107_b200 import ReuseViT, plan_gop
+    from paper_2506_14107_b200.dist import combine_plans, lpt_assign, reuse_estimate
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS["l14_336"]
+    L, N, D = cfg.layers, cfg.N, cfg.dim
+    ps = [(0.05, 0.1, 0.2, 0.4)[v % 4] for v in range(args.videos)]
+    costs = [args.video_frames * (1.0 - reuse_estimate(p, T=cfg.T, N=N)) for p in ps]
+    assign = lpt_assign(costs, world)
+    mine = assign[rank]
+    xs, cs = [], []
+    for v in mine:
+        x, c = synth.make_video_torch(cfg, args.video_frames, ps[v], seed=5000 + v, device=dev)
+        xs.append(x)
+        cs.append(c)
+    cp = combine_plans([plan_gop(args.video_frames, args.refresh) for _ in mine])
+    plan = {k: cp[k] for k in ("type", "past", "future", "order")}
+    x = torch.cat(xs).contiguous()
+    c = torch.cat(cs).contiguous()
+    del xs, cs
+    n_loc = x.shape[0]
+    W = synth.make_vit(cfg)
+    G = synth.make_gates(cfg)
+    m = ReuseViT(cfg, local)
+    m.load_vit(synth.pack_vit(cfg, W))
+    m.load_gates(synth.pack_gates(cfg, G))
+    emb = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
+    masks = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    n_max = max(len(a) for a in assign) * args.video_frames
+    zp = torch.zeros((n_max, D), dtype=torch.float32, device=dev)
+    zg = torch.empty((world * n_max, D), dtype=torch.float32, device=dev)
+
+    def step():
+        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream)
+        st = m.wait()
+        if world > 1:
+            zp[:n_loc] = emb
+            dist.all_gather_into_tensor(zg, zp)
+        return st
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        st = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    loads = [sum(costs[v] for v in a) for a in assign]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_total = args.videos * args.video_frames
+    line = {"metric": "ViT-L/14@336 ReuseViT multi-video embedding frames/sec (64 videos x 120 frames)",
+            "value": n_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "CLIP ViT-L/14 336px (T=577) ReuseViT, 64 videos x 120 frames (BASELINE "
+                                   "configs[4]), per-video motion p in {.05,.1,.2,.4}, LPT sharding by estimated cost",
+                       "frames": n_total, "videos_per_gpu": [len(a) for a in assign],
+                       "est_load_per_gpu": [round(v, 1) for v in loads],
+                       "load_imbalance": max(loads) / (sum(loads) / world),
+                       "parallelism": f"video-group dp{world}", "seq_len": cfg.T},
+            "reuse": {"reuse_all": st["reuse_all"], "reuse_nonI": st["reuse_nonI"]},
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.out:
+            with open(args.out, "w") as fh:
+                fh.write(json.dumps(line) + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "c5":
+        run_c5(args)
         return
     import numpy as np
     import torch

@@ -68,3 +68,106 @@ def embed_sharded(model, patches, codec, refresh: int = 20, group=None, **embed_
         parts_z.append(zg[r * n_max:r * n_max + n_r])
         parts_m.append(mg[r * n_max:r * n_max + n_r])
     return torch.cat(parts_z), torch.cat(parts_m)
+
+
+# ------------------------------------------------------------------ multi-video
+def reuse_estimate(p_motion: float, refresh: int = 20, T: int = 257, N: int = 256) -> float:
+    """Expected reuse_all of the SPEC plan for per-step patch motion probability p (SURVEY §8(d)
+    derivation: P frames (1-p)^4, B2 1-(1-(1-p)^2)^2, B1 1-p^2, weights 4:5:10 per 19 non-I
+    frames of a 20-frame group, CLS never reused).  Used only to balance work across GPUs."""
+    q = 1.0 - p_motion
+    rp, rb2, rb1 = q ** 4, 1.0 - (1.0 - q * q) ** 2, 1.0 - p_motion ** 2
+    non_i = (4 * rp + 5 * rb2 + 10 * rb1) / 19.0
+    return non_i * (refresh - 1) / refresh * N / T
+
+
+def lpt_assign(costs, world: int):
+    """Longest-processing-time-first assignment of independent videos to `world` ranks
+    (C5 balances by estimated cost sum(1 - r_hat) per video).  Returns, per rank,
+    the video indices in ascending order (videos stay whole on one GPU; no halo needed)."""
+    if world < 1:
+        raise ValueError("world >= 1")
+    loads = [0.0] * world
+    out = [[] for _ in range(world)]
+    for v in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        out[r].append(v)
+        loads[r] += costs[v]
+    return [sorted(o) for o in out]
+
+
+def combine_plans(plans):
+    """Block-diagonal plan for several independent videos embedded in one call: frame indices
+    of video k are offset by the frames before it, references stay inside each video, and the
+    computation order is the videos' orders one after another (every reference still precedes
+    its dependents).  The runtime then batches equal dependency levels across all videos."""
+    import numpy as np
+    offs, acc = [], 0
+    for p in plans:
+        offs.append(acc)
+        acc += len(p["type"])
+    shift = lambda a, o: np.where(np.asarray(a) >= 0, np.asarray(a) + o, -1).astype(np.int32)
+    return {"type": np.concatenate([np.asarray(p["type"], np.int8) for p in plans]),
+            "past": np.concatenate([shift(p["past"], o) for p, o in zip(plans, offs)]),
+            "future": np.concatenate([shift(p["future"], o) for p, o in zip(plans, offs)]),
+            "order": np.concatenate([np.asarray(p["order"], np.int32) + o for p, o in zip(plans, offs)]),
+            "offsets": np.asarray(offs + [acc], np.int64)}
+
+
+def embed_videos(model, videos, refresh: int = 20, **embed_kw):
+    """Embed several independent videos [(patches [n_k, N, pp], codec [n_k, N]), ...] in ONE
+    rv_embed with the combined plan (bigger level waves than one call per video).  Returns the
+    per-video (Z, masks) in input order."""
+    import torch
+    from .api import plan_gop
+    plans = [plan_gop(int(x.shape[0]), refresh) for x, _ in videos]
+    cp = combine_plans(plans)
+    xs = torch.cat([torch.as_tensor(x) for x, _ in videos]).contiguous()
+    cs = torch.cat([torch.as_tensor(c) for _, c in videos]).contiguous()
+    plan = {k: cp[k] for k in ("type", "past", "future", "order")}
+    Z, M, _, _ = model.embed(xs, cs, plan, **embed_kw)
+    Z, M = torch.as_tensor(Z), torch.as_tensor(M)
+    o = cp["offsets"]
+    return [(Z[o[k]:o[k + 1]], M[o[k]:o[k + 1]]) for k in range(len(videos))]
+
+
+def embed_videos_sharded(model, videos, costs=None, refresh: int = 20, group=None, **embed_kw):
+    """C5 on `world` GPUs: videos assigned to ranks by LPT on their estimated cost (default:
+    frame count), each rank embeds its videos in one call, embeddings all-gathered (NCCL;
+    gloo in the CPU tests).  Returns the list of per-video Z on every rank, in input order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lens = [int(x.shape[0]) for x, _ in videos]
+    if costs is None:
+        costs = [float(n) for n in lens]
+    assign = lpt_assign(costs, world)
+    mine = assign[rank]
+    outs = embed_videos(model, [videos[v] for v in mine], refresh, **embed_kw) if mine else []
+    if world == 1:
+        return [z for z, _ in outs]
+    D = None
+    for z, _ in outs:
+        D = z.shape[1]
+    if D is None:
+        D = int(model.cfg.dim)
+    dev = outs[0][0].device if outs else torch.device("cpu")
+    dt = outs[0][0].dtype if outs else torch.float32      # fp32 from libreusevit
+    n_rank = [sum(lens[v] for v in a) for a in assign]
+    n_max = max(n_rank)
+    zp = torch.zeros((n_max, D), dtype=dt, device=dev)
+    if outs:
+        zp[:n_rank[rank]] = torch.cat([z for z, _ in outs])
+    zg = torch.empty((world * n_max, D), dtype=dt, device=dev)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(zg, zp, group=group)
+    else:
+        dist.all_gather(list(zg.chunk(world)), zp, group=group)
+    res = [None] * len(videos)
+    for r in range(world):
+        off = r * n_max
+        for v in assign[r]:
+            res[v] = zg[off:off + lens[v]]
+            off += lens[v]
+    return res

@@ -89,3 +89,95 @@ def test_embed_sharded_gloo_world2():
     x, c = synth.make_video(cfg, 41, 0.3, seed=2001)
     ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(41))
     assert np.array_equal(Z, ref["Z"]) and np.array_equal(M, ref["M"])
+
+
+# ------------------------------------------------------------------ multi-video (C5) sharding
+import itertools  # noqa: E402
+
+from paper_2506_14107_b200.dist import combine_plans, lpt_assign, reuse_estimate  # noqa: E402
+
+
+def test_reuse_estimate_matches_survey_table():
+    """SURVEY §8(d) reuse sweep (derived from the plan): reuse_all at p = 1 .. 0."""
+    table = {1.0: 0.00, 0.6: 0.40, 0.4: 0.59, 0.3: 0.69, 0.2: 0.78, 0.1: 0.86, 0.05: 0.91, 0.0: 0.946}
+    for p, r in table.items():
+        assert abs(reuse_estimate(p) - r) < 0.006, (p, reuse_estimate(p), r)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lpt_within_graham_bound(seed):
+    """Every video on exactly one rank; makespan within LPT's 4/3 - 1/(3m) of the optimum
+    (brute force over all assignments of 8 videos to 3 ranks)."""
+    rng = np.random.default_rng(seed)
+    costs = list(rng.uniform(1, 10, 8))
+    m = 3
+    a = lpt_assign(costs, m)
+    assert sorted(v for r in a for v in r) == list(range(8))
+    mk = max(sum(costs[v] for v in r) for r in a)
+    opt = min(max(sum(c for c, k in zip(costs, asg) if k == r) for r in range(m))
+              for asg in itertools.product(range(m), repeat=8))
+    assert mk <= (4 / 3 - 1 / (3 * m)) * opt + 1e-9
+
+
+def test_combined_plan_is_block_diagonal_and_valid():
+    plans = [oracle.plan_gop(n) for n in (21, 5, 40, 1)]
+    cp = combine_plans(plans)
+    n = int(cp["offsets"][-1])
+    assert sorted(cp["order"].tolist()) == list(range(n))
+    pos = {int(f): i for i, f in enumerate(cp["order"])}
+    for k, p in enumerate(plans):
+        o0, o1 = int(cp["offsets"][k]), int(cp["offsets"][k + 1])
+        for f in range(o0, o1):
+            assert cp["type"][f] == p["type"][f - o0]
+            for key in ("past", "future"):
+                r = int(cp[key][f])
+                assert (r == -1) == (p[key][f - o0] == -1)
+                if r >= 0:
+                    assert o0 <= r < o1 and pos[r] < pos[f]
+    # the oracle's level-batched schedule of the combined plan (S:410 math-neutral batching)
+    lev = oracle.plan_levels({k: cp[k] for k in ("type", "past", "future", "order")})
+    assert len(lev) == n
+
+
+def _worker_videos(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_14107_b200 import dist as rvdist
+    import paper_2506_14107_b200.api as api
+    api.plan_gop = lambda n, refresh=20, reorder=True: oracle.plan_gop(n, refresh, reorder)
+    cfg = synth.CONFIGS["tiny"]
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=True)
+    vids = []
+    for k, (n, p) in enumerate([(9, 0.1), (5, 0.4), (12, 0.2)]):
+        x, c = synth.make_video(cfg, n, p, seed=2100 + k)
+        vids.append((torch.from_numpy(x), torch.from_numpy(c)))
+    costs = [x.shape[0] * (1 - rvdist.reuse_estimate(p)) for (x, _), p in zip(vids, [0.1, 0.4, 0.2])]
+    Zs = rvdist.embed_videos_sharded(OracleModel(cfg, W, G), vids, costs=costs)
+    if rank == 0:
+        q.put([z.numpy() for z in Zs])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_embed_videos_sharded_gloo_world2():
+    """C5: independent videos LPT-assigned to 2 ranks, one combined-plan embed per rank,
+    gathered per video == each video embedded alone (fp64 oracle as the per-rank model)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_videos, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    Zs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    cfg = synth.CONFIGS["tiny"]
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=True)
+    for k, (n, p) in enumerate([(9, 0.1), (5, 0.4), (12, 0.2)]):
+        x, c = synth.make_video(cfg, n, p, seed=2100 + k)
+        ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(n))
+        np.testing.assert_allclose(Zs[k], ref["Z"], rtol=0, atol=1e-12)

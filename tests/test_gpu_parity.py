@@ -225,3 +225,28 @@ def test_duplicate_frame_reuses_everything(cuda_ok):
     Zc = Z.cpu().double()
     cos = (Zc[4] @ Zc[0]) / Zc[4].norm() / Zc[0].norm()
     assert cos.item() >= 0.999
+
+
+@pytest.mark.parametrize("cfgname", ["b16", "l14_336"])
+def test_multi_video_embed_equals_per_video(cuda_ok, cfgname):
+    """several independent videos embedded in ONE call with the combined
+    block-diagonal plan (level waves span the videos) reproduce each video's own embed bit for
+    bit (batch-invariant kernels), and match the fp64 oracle."""
+    from paper_2506_14107_b200.dist import embed_videos
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    specs = [(9, 0.1), (5, 0.4), (12, 0.2)]
+    vids = []
+    for k, (n, p) in enumerate(specs):
+        x, c = synth.make_video(cfg, n, p, seed=4100 + k)
+        vids.append((torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()))
+    outs = embed_videos(m, vids)
+    torch.cuda.synchronize()
+    for k, (x, c) in enumerate(vids):
+        Z1, M1, _, _ = m.embed(x, c)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[k][0], Z1) and torch.equal(outs[k][1], M1), k
+    x, c = synth.make_video(cfg, 5, 0.4, seed=4101)
+    ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(5))
+    err, cos = metrics(outs[1][0].cpu().numpy(), ref["Z"])
+    assert err.max() <= 2e-2 and cos.min() >= 0.999
