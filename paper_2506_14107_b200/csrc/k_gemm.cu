@@ -7,7 +7,8 @@
 // no host synchronisation is needed between compaction and the contractions
 // and the whole layer loop is CUDA-graph capturable.
 //
-// CTA = 320 threads, one CTA per SM (persistent over 128 x BN output tiles):
+// CTA = 320 threads, one CTA per SM (persistent over 128 x BN output tiles; BN = 256 GEMMs run
+// as CTA pairs over 256 x 256 tiles with tcgen05.mma.cta_group::2, see Cfg::PAIR):
 //   warp 0 : TMA producer (one elected lane), STAGES-deep smem ring, SWIZZLE_128B tiles
 //   warp 1 : MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
 //   warp 1 also allocates TMEM (2*BN fp32 columns: double-buffered accumulator)
@@ -43,15 +44,21 @@ constexpr int RDEPTH = 2;         // residual chunks in flight per epilogue warp
 // freed shared memory holds a cp.async ring of residual rows RDEPTH chunks deep; the chunk's
 // ring slot doubles as its transpose tile once the residual is in registers, so the HBM-bound
 // epilogue keeps 128 KB of residual loads in flight per SM.
-template <int BN, int MODE>
+// PAIR: a CTA pair on one TPC (cluster of 2) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A and half of the BN
+// rows of B, the leader CTA issues the MMAs, each CTA's TMEM holds its 128 accumulator rows.
+// Half the B bytes per CTA -> more mainloop stages in the same shared memory.
+template <int BN, int MODE, bool PAIR = false>
 struct Cfg {
   static constexpr bool SR = MODE == 1;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = SR ? 2 : MODE == 2 ? 3 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  static constexpr int STAGES = PAIR ? (MODE == 2 ? 4 : (BN == 256 ? 6 : 8))
+                                     : SR ? 2 : MODE == 2 ? 3 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int EPI = epi_warps<BN, MODE>();
+  static constexpr int TILE_M = PAIR ? 2 * BM : BM;
   // per-warp 32x32 fp32 transpose tile + row maps (SR: output rows only; the ring slot is the
   // tile and the residual rows travel by shuffle)
   static constexpr int STAGE_OUT = SR ? EPI * 32 * 4 : EPI * (32 * 32 + 64) * 4;
@@ -106,6 +113,45 @@ RV_DEV float4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
   return v;
 }
+// ---- CTA-pair (cluster of 2) helpers
+RV_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+RV_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+RV_DEV uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+RV_DEV void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+}
+// TMA load into this CTA's shared memory, completion counted on the leader CTA's barrier
+RV_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(bar_cl)
+      : "memory");
+}
+RV_DEV void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the MMAs retire
+RV_DEV void mma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
 RV_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 RV_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -118,9 +164,9 @@ RV_DEV uint64_t smem_desc_sw128(const void* p) {
 }
 // Instruction descriptor for kind::f16: D fp32 (bits 4-5 = 1), A bf16 (7-9 = 1), B bf16
 // (10-12 = 1), both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-template <int BN>
+template <int BN, int MM = BM>
 __host__ __device__ constexpr uint32_t idesc_bf16() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(MM >> 4) << 24);
 }
 RV_DEV void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -156,11 +202,11 @@ RV_DEV float quick_gelu_fast(float x) {
   return x * fmaf(0.5f, t, 0.5f);
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool PAIR>
 __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
-  using C = Cfg<BN, MODE>;
+  using C = Cfg<BN, MODE, PAIR>;
   constexpr bool SR = C::SR;
   extern __shared__ __align__(1024) uint8_t smem_raw[];   // SWIZZLE_128B needs 1024-B aligned stages
   uint8_t* smem = smem_raw;
@@ -177,8 +223,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = M_dev ? *M_dev : M_host;
   const int tiles_n = N / BN;
-  const int ntiles = ((M + BM - 1) / BM) * tiles_n;
+  const int ntiles = ((M + C::TILE_M - 1) / C::TILE_M) * tiles_n;
   const int nk = K / BK;
+  // PAIR: the pair (cluster) index walks the tiles; rank 1 holds rows 128..255 of each tile
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -189,17 +239,24 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], C::EPI * 32);
+      mbar_init(&tempty[a], PAIR ? 2 * C::EPI : C::EPI * 32);   // PAIR: one arrive per warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  __syncwarp();
+  if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -207,24 +264,33 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
         const int mb = tile / tiles_n, nb = tile % tiles_n;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+          if constexpr (PAIR) {
+            const uint32_t fb = mapa_rank(&full[stage], 0);   // the leader's barrier counts both CTAs
+            // leader: its own barrier, CTA-scope arrive (a .release.cluster arrive costs a
+            // MEMBAR + ERRBAR per k-step and serialises the TMA ring: measured 2x slower)
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, mb * C::TILE_M + (int)rank * BM);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, nb * BN + (int)rank * (BN / 2));
+          } else {
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16<BN>();
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16<BN, C::TILE_M>();
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      for (int tile = tile0; tile < ntiles; tile += tstep, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -236,12 +302,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
           const uint64_t ad = smem_desc_sw128(sA + stage * C::A_BYTES);
           const uint64_t bd = smem_desc_sw128(sB + stage * C::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the 128 B swizzle atom
-            mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          mma_commit(&empty[stage]);          // frees the smem slot once these MMAs retire
+          for (int k = 0; k < BK / 16; ++k) {   // +32 B along K inside the 128 B swizzle atom
+            if constexpr (PAIR) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (PAIR) mma_commit_pair(&empty[stage]);   // frees the slot in both CTAs
+          else mma_commit(&empty[stage]);     // frees the smem slot once these MMAs retire
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);              // accumulator ready for the epilogue
+        if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
+        else mma_commit(&tfull[acc]);         // accumulator ready for the epilogue
       }
     }
   } else if (warp >= 2) {
@@ -261,11 +331,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     const int rsub = lane >> 3;          // row within a group of 4
     const int c4 = (lane & 7) * 4;       // first of this lane's 4 columns
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int tile = tile0; tile < ntiles; tile += tstep, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int mb = tile / tiles_n, nb = tile % tiles_n;
-      const int row0 = mb * BM + q * 32;
+      const int row0 = mb * C::TILE_M + (int)rank * BM + q * 32;
       // per-tile row maps (lane = row within this warp's 32 rows), kept in shared memory
       {
         const int m = row0 + lane;
@@ -387,14 +457,24 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl(mapa_rank(&tempty[acc], 0));
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  __syncwarp();
+  // PAIR: no CTA leaves while its partner may still signal its barriers or read its smem
+  if constexpr (PAIR) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
   }
 }
 
@@ -447,7 +527,7 @@ cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max
   using C = Cfg<BN, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            C::SMEM);
     if (err != cudaSuccess) return err;
     attr = true;
@@ -455,8 +535,51 @@ cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, MODE><<<grid, gemm_threads<BN, MODE>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+  gemm_tc_kernel<BN, MODE, false><<<grid, gemm_threads<BN, MODE>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
   return cudaGetLastError();
+}
+
+// CTA-pair launch: clusters of 2 (one TPC), grid = 2 x min(tiles, SMs / 2)
+template <int BN, int MODE>
+cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
+  using C = Cfg<BN, MODE, true>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           C::SMEM);
+    if (err != cudaSuccess) return err;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(gemm_threads<BN, MODE>());
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // persistent: only as many pairs as can be co-resident (TPC pairing can leave SMs unpaired;
+  // a second wave of pairs would double the time of the tiles they own)
+  static int max_pairs = 0;
+  if (!max_pairs) {
+    cfg.gridDim = dim3(num_sms() & ~1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, MODE, true>, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    max_pairs = n < num_sms() / 2 ? n : num_sms() / 2;
+    if (getenv("RV_GEMM_DEBUG")) fprintf(stderr, "[gemm] BN=%d MODE=%d: %d co-resident CTA pairs\n", BN, MODE, n);
+  }
+  const int tiles = ((max_m + C::TILE_M - 1) / C::TILE_M) * (p.N / BN);
+  int pairs = max_pairs;
+  if (tiles < pairs) pairs = tiles;
+  if (pairs < 1) pairs = 1;
+  cfg.gridDim = dim3(2 * pairs);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE, true>, p.tmA, p.tmB2, M_dev, M_host, p.N, p.K, e);
 }
 
 template <int BN>
@@ -466,7 +589,19 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   // with K <= 1024 (W_o): 16 epilogue warps, 3 stages (tools/r2_bench.py: 57 -> 52 us on a
   // 16k-row W_o; FC2's K = 4096 mainloop needs its 4 stages).  RV_GEMM_RE=0 disables.
   static const bool re_on = !getenv("RV_GEMM_RE") || atoi(getenv("RV_GEMM_RE")) != 0;
+  // RV_GEMM_PAIR: 0 off, 1 (default) CTA pairs (256 x 256 tiles) for the MODE 0 / 2 GEMMs with
+  // BN = 256 (tools/gemm_bench.py at M = 80k: QKV 432 -> 385 us, FC1 572 -> 521, FC2 508 -> 464,
+  // W_o 193 -> 154; in the bench FC2 67 -> 60 ms per step); R1 (N = 128) stays single-CTA
+  // (17 -> 20 ms as pairs: half as many 256-row tiles on small waves)
+  static const int pair_on = getenv("RV_GEMM_PAIR") ? atoi(getenv("RV_GEMM_PAIR")) : 1;
   if (p.K <= 2 * BK && e.resid) return launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
+  if constexpr (BN == 256) {
+    if (pair_on) {
+      if (re_on && p.K <= 1024 && (e.resid ? BN >= 128 : BN == 256))
+        return launch_pair<BN, 2>(p, M_dev, M_host, max_m, e, s);
+      return launch_pair<BN, 0>(p, M_dev, M_host, max_m, e, s);
+    }
+  }
   // 16-warp epilogue: W_o (gathered residual, BN >= 128) and the wide bf16-output GEMMs with
   // K <= 1024 (QKV with its K/V scatter, FC1 with QuickGELU: 65 -> 57 and 82 -> 73 ms per step);
   // not R1 (N = 128: one N tile, slower)
@@ -491,7 +626,8 @@ bool gemm_make_plan(GemmPlan* p, const void* A, long long a_rows, const void* B,
   p->N = N;
   p->K = K;
   p->BN = (N % 256 == 0 && bn_max >= 256) ? 256 : ((N % 128 == 0 && bn_max >= 128) ? 128 : 64);
-  return encode_2d(&p->tmA, A, a_rows, K, BM, err, errlen) && encode_2d(&p->tmB, B, N, K, p->BN, err, errlen);
+  return encode_2d(&p->tmA, A, a_rows, K, BM, err, errlen) && encode_2d(&p->tmB, B, N, K, p->BN, err, errlen) &&
+         encode_2d(&p->tmB2, B, N, K, p->BN >= 128 ? p->BN / 2 : p->BN, err, errlen);
 }
 
 cudaError_t gemm_launch(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,

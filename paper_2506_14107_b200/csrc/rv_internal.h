@@ -35,6 +35,7 @@ struct Epi {
 struct GemmPlan {
   CUtensorMap tmA;        // A bf16 [rows][K], box {64, 128}, SWIZZLE_128B
   CUtensorMap tmB;        // B bf16 [N][K],    box {64, BN},  SWIZZLE_128B
+  CUtensorMap tmB2;       // B bf16 [N][K],    box {64, BN/2} (CTA-pair GEMM: half of B per CTA)
   int N = 0, K = 0, BN = 0;
 };
 
