@@ -128,8 +128,10 @@ RV_DEV uint32_t mapa_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// remote arrive with the default (.release.cta) semantics, as CUTLASS's ClusterBarrier::arrive:
+// .release.cluster would add a MEMBAR + ERRBAR that waits for the warp's epilogue stores
 RV_DEV void mbar_arrive_cl(uint32_t bar_cl) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
 }
 // TMA load into this CTA's shared memory, completion counted on the leader CTA's barrier
 RV_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl, int x, int y) {

@@ -72,6 +72,12 @@ struct rv_ctx {
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
   bf16* dfull = nullptr;      // [max_w][T][D] Delta of reused tokens (wave-local token rows, bf16)
   int* rpos = nullptr;        // [max_w][T] compact restoration row of token w*T+i (-1: recomputed)
+  // fused score + R1 (k_score_r1.cu): hr of reused tokens at their wave-local rows, and R2's
+  // per-row maps over all wave-local rows (output row or -1; the provider's row)
+  bf16* hr_full = nullptr;    // [max_w][T][Hr]
+  int *r2_out = nullptr, *r2_res = nullptr;   // [max_w][T]
+  bool fuse_r1 = false;
+  std::vector<CUtensorMap> tm_wr1;   // Wr1 [Hr][D], box {64, Hr}
   bf16* patches_bf16 = nullptr;
   float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
   uint8_t* out_masks = nullptr;
@@ -95,7 +101,7 @@ struct rv_ctx {
   GemmPlan pe;
   CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
   CUtensorMap tmKV;                // K/V cache [n T][2 D], box {64, 1}: row gathers (tcgen05 attention)
-  std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
+  std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2, g_r2f;
   // ---- graph cache
   cudaGraphExec_t gexec = nullptr;
   std::vector<long long> gkey;
@@ -282,6 +288,9 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->kvsrc, n * T);
   AL(ctx->dfull, (size_t)max_w * T * D);
   AL(ctx->rpos, max_w * T);
+  AL(ctx->hr_full, (size_t)max_w * T * ctx->Hr);
+  AL(ctx->r2_out, max_w * T);
+  AL(ctx->r2_res, max_w * T);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
   AL(ctx->in_patches, (size_t)n * N * ctx->pp);
   AL(ctx->in_codec, n * N);
@@ -306,7 +315,8 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->reuse_ctr, 64);
 #undef AL
   // the restoration GEMMs also read the never-written Delta rows of C tokens (results discarded)
-  if (cudaMemset(ctx->dfull, 0, (size_t)max_w * T * D * sizeof(bf16)) != cudaSuccess)
+  if (cudaMemset(ctx->dfull, 0, (size_t)max_w * T * D * sizeof(bf16)) != cudaSuccess ||
+      cudaMemset(ctx->hr_full, 0, (size_t)max_w * T * ctx->Hr * sizeof(bf16)) != cudaSuccess)
     return fail(ctx, RV_ECUDA, "cudaMemset failed");
   ctx->n_cap = n;
   ctx->capC = capC;
@@ -324,7 +334,12 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   const int bn_resid = getenv("RV_BN_RESID") ? atoi(getenv("RV_BN_RESID")) : 256;
   const int bn_r2 = getenv("RV_BN_R2") ? atoi(getenv("RV_BN_R2")) : 256;
   ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
-  ctx->g_r1.resize(L); ctx->g_r2.resize(L);
+  ctx->g_r1.resize(L); ctx->g_r2.resize(L); ctx->g_r2f.resize(L); ctx->tm_wr1.resize(L);
+  // RV_SCORE_R1=1: fused score + R1 (k_score_r1.cu).  Off by default: correct (the whole -m gpu
+  // suite passes with it, bitwise equal outputs) but 201 ms per step vs 83 + 17 unfused -- its
+  // 128 KB A tile leaves one 16-warp CTA per SM, a quarter of the score kernel's loads in flight
+  static const bool fuse_env = getenv("RV_SCORE_R1") && atoi(getenv("RV_SCORE_R1")) != 0;
+  ctx->fuse_r1 = fuse_env && ctx->gates_loaded && score_r1_supported((int)D, ctx->Hr);
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
     bool ok = gemm_make_plan(&ctx->g_qkv[l], ctx->A, capC, w.Wqkv, 3 * (int)D, (int)D, e, sizeof e) &&
@@ -334,6 +349,9 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
     if (ok && ctx->gates_loaded)
       ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
            gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
+    if (ok && ctx->fuse_r1)
+      ok = make_tmap_bf16(&ctx->tm_wr1[l], w.Wr1, ctx->Hr, (int)D, ctx->Hr, e, sizeof e) &&
+           gemm_make_plan(&ctx->g_r2f[l], ctx->hr_full, max_w * T, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
     if (!ok) return fail(ctx, RV_ECUDA, "%s", e);
   }
   return RV_OK;
@@ -402,12 +420,19 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       const int n_w = wv.n_w;
       const int* wd = ctx->wdesc + (size_t)wv.off * 4;
       const int maxC = n_w * T;
-      // a2-a3: Eq. 1-4
+      // a2-a3: Eq. 1-4 (fused with R1 of a12 when the wave restores anything)
+      const bool fused = ctx->fuse_r1 && wv.any_ref && !dense;
       r.begin(K_SCORE,l,wi);
-      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
-                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
-                         ctx->wprov, ctx->cntR, ctx->dfull, s),
-            "score");
+      if (fused)
+        r.chk(launch_score_r1(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr, w.gate,
+                              ctx->Hg, masks, scores, ctx->wmask, ctx->wprov, ctx->cntR, &ctx->tm_wr1[l], w.br1,
+                              ctx->hr_full, ctx->r2_out, ctx->r2_res, s),
+              "score_r1");
+      else
+        r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
+                           ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
+                           ctx->wprov, ctx->cntR, ctx->dfull, s),
+              "score");
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
@@ -484,8 +509,20 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       // a12: restoration (Eq. 9) + merge (Eq. 10, R side).  The score pass wrote Delta (Eq. 8)
       // into the wave-local token rows w*T+i; R1 reads them in place over all n_w*T rows and
       // stores only the reused rows, compacted (row map rpos; -1 for C rows): no Delta copy.
-      // R2 runs over the M_R compact rows.
-      if (wv.any_ref && !dense) {
+      // R2 runs over the M_R compact rows.  Fused: R1 ran inside the score pass; R2 runs over
+      // all n_w * T wave-local rows of hr with the score pass's row maps (-1: not reused).
+      if (fused) {
+        Epi e2;
+        e2.bias = w.br2;
+        e2.resid = Xout;
+        e2.resid_rows = ctx->r2_res;
+        e2.resid_ld = D;
+        e2.out = Xout;
+        e2.out_rows = ctx->r2_out;
+        e2.out_ld = D;
+        r.begin(K_R2,l,wi);
+        r.chk(gemm_launch(ctx->g_r2f[l], nullptr, n_w * T, n_w * T, e2, s), "gemm_r2");
+      } else if (wv.any_ref && !dense) {
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;

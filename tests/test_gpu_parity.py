@@ -5,6 +5,8 @@ the same seeded inputs (BASELINE.json north star tolerances, SURVEY D10 metric f
   * reuse masks agree on >= 99.9% of tokens with |d_oracle| >= 1e-3
 plus invariants that hold bitwise on the GPU (forced all-reuse P-frame, determinism,
 graph vs direct launches, host vs device pointers)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -13,6 +15,7 @@ import oracle
 import synth
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def metrics(Zg, Zr):
@@ -250,3 +253,41 @@ def test_multi_video_embed_equals_per_video(cuda_ok, cfgname):
     ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(5))
     err, cos = metrics(outs[1][0].cpu().numpy(), ref["Z"])
     assert err.max() <= 2e-2 and cos.min() >= 0.999
+
+
+_FUSED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_2506_14107_b200 import ReuseViT
+cfg = synth.CONFIGS[sys.argv[2]]
+W, G = synth.make_vit(cfg), synth.make_gates(cfg)
+m = ReuseViT(cfg, 0)
+m.load_vit(synth.pack_vit(cfg, W))
+m.load_gates(synth.pack_gates(cfg, G))
+x, c = synth.make_video(cfg, 41, 0.3, seed=21)
+Z, M, _, _ = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda())
+torch.cuda.synchronize()
+np.save(sys.argv[3], np.concatenate([Z.cpu().numpy().view(np.uint32).ravel().astype(np.int64),
+                                     M.cpu().numpy().ravel().astype(np.int64)]))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfgname", ["b16", "l14"])
+def test_fused_score_r1_bitwise_equal(cuda_ok, cfgname, tmp_path):
+    """The opt-in fused decision + R1 kernel (RV_SCORE_R1=1, k_score_r1.cu) computes the same
+    fp32 decision arithmetic and the same bf16 Delta / K order as score_kernel + the R1 GEMM:
+    embeddings and masks are bitwise equal to the default path (run in subprocesses because the
+    switch is read once per process)."""
+    import subprocess
+    import sys
+    outs = []
+    for flag in ("0", "1"):
+        f = tmp_path / f"out{flag}.npy"
+        env = dict(os.environ, RV_SCORE_R1=flag)
+        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, ROOT, cfgname, str(f)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
