@@ -42,8 +42,14 @@ constexpr int A8_LOADERS = 64;                 // cp.async lanes (warps 0-1)
 constexpr int A8_QROWS = 64;                   // M of both MMAs
 constexpr int A8_MAXK = 256;                   // patch keys per item
 constexpr int A8_MAX_TILES = 5;                // T <= 257 -> <= 257 compact queries per frame
-constexpr int A8_NKT = 2;                      // K tile ring slots
-constexpr int A8_NVT = 3;                      // V tile ring slots
+#ifndef A8_NKT_SLOTS
+#define A8_NKT_SLOTS 2
+#endif
+#ifndef A8_NVT_SLOTS
+#define A8_NVT_SLOTS 3
+#endif
+constexpr int A8_NKT = A8_NKT_SLOTS;           // K tile ring slots
+constexpr int A8_NVT = A8_NVT_SLOTS;           // V tile ring slots
 constexpr int A8_NT = A8_NKT + A8_NVT;
 #ifndef A8_NQ_SLOTS
 #define A8_NQ_SLOTS 4

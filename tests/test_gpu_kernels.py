@@ -36,7 +36,9 @@ def _model(cfg, gates=True, **gk):
 # ------------------------------------------------------------------------- GEMM
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (100, 192, 64), (128, 256, 1024), (300, 768, 768),
                                    (1000, 3072, 1024), (4097, 1024, 4096), (257, 128, 1024),
-                                   (513, 1024, 128), (20000, 4096, 1024)])
+                                   (513, 1024, 128), (20000, 4096, 1024),
+                                   # CTA-pair path (BN = 256): a lone row, rank 1 holding 1 row, ragged tails
+                                   (1, 256, 64), (129, 1024, 256), (383, 512, 4096), (70001, 1024, 1024)])
 def test_gemm_vs_torch(dev, M, N, K):
     m, _, _ = _model(synth.CONFIGS["tiny"], gates=False)
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N + K)
