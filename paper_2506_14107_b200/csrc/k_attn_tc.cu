@@ -54,6 +54,13 @@ constexpr int A8_NT = A8_NKT + A8_NVT;
 #ifndef A8_NQ_SLOTS
 #define A8_NQ_SLOTS 4
 #endif
+// A8_PAIR_PV: items come in head pairs (h, h+1) of the same frame and query tile; their P V is
+// one M = 128, N = 128 MMA per 16 keys (P of both items in the two TMEM lane halves, V of both
+// heads as one MN-major operand over two adjacent V slots), 16 instead of 32 instructions
+#ifndef A8_PAIR_PV
+#define A8_PAIR_PV 0
+#endif
+static_assert(!A8_PAIR_PV || A8_NVT_SLOTS % 2 == 0, "pair P V needs an even V ring");
 constexpr int A8_NQ = A8_NQ_SLOTS;             // Q ring slots (items the loader may run ahead)
 constexpr uint32_t A8_TILE = A8_MAXK * 128;    // 256 keys x 128 B
 // Q tile, then the CLS key's K row at +8192 (row 0 of a 1 KB swizzle atom: unswizzled) and its
@@ -139,9 +146,13 @@ RV_DEV uint64_t sdesc(uint32_t addr) {
 }
 // kind::f16 instruction descriptor: D fp32, A/B bf16, A K-major, B K-major (b_mn = 0) or
 // MN-major (b_mn = 1), N >> 3 at bit 17, M >> 4 at bit 24 (M = 64).
-RV_DEV uint32_t idesc64(int N, int b_mn) {
+RV_DEV uint32_t idesc64(int N, int b_mn, int M = A8_QROWS) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(A8_QROWS >> 4) << 24);
+         ((uint32_t)(M >> 4) << 24);
+}
+// MN-major operand spanning two 64-wide N blocks `lbo` bytes apart (leading byte offset)
+RV_DEV uint64_t sdesc_lbo(uint32_t addr, uint32_t lbo) {
+  return sdesc(addr) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
 }
 // 16x32bx2 shapes: lanes 0-15 access TMEM lanes base..base+15 at columns [c, c+n), lanes 16-31
 // the same TMEM lanes at columns [c+OFF, c+OFF+n).
@@ -299,8 +310,10 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
     // ======================================================================== loaders
     // Item slots it = blockIdx.x + k * gridDim.x over (qt, w, h), qt slowest: the first n_w*H
     // slots (tile 0 of every frame-head) are all live; later tiles exist for large frames only.
-    const long long n_items = (long long)n_w * H * A8_MAX_TILES;
-    const long long per_t = (long long)n_w * H;
+    constexpr int HP = A8_PAIR_PV ? 2 : 1;        // heads per item slot
+    const int Hs = H / HP;
+    const long long n_items = (long long)n_w * Hs * A8_MAX_TILES;
+    const long long per_t = (long long)n_w * Hs;
     const long long ld = 2LL * D;
     const int half = warp;          // this warp gathers patch keys [128 half, 128 half + 128)
     uint32_t kseq = 0, vseq = 0;    // K / V tile sequence numbers
@@ -316,8 +329,8 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
         if (my < n_items) {
           b_qt = (int)(my / per_t);
           const int rem = (int)(my - (long long)b_qt * per_t);
-          const int w = rem / H;
-          b_h = rem - w * H;
+          const int w = rem / Hs;
+          b_h = (rem - w * Hs) * HP;
           const int a = __ldg(qoff + w), nq = __ldg(qoff + w + 1) - a;
           live = b_qt * A8_QROWS < nq;
           b_q0 = a + b_qt * A8_QROWS;
@@ -382,29 +395,40 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       int n_q0 = 0, n_nr = 0, n_sl = 0, n_h = 0, n_qt = 0, nrows_[4];
       const bool nhave = next_item(n_q0, n_nr, n_sl, n_h, n_qt);
       if (nhave) load_rows(n_sl, nrows_);
-      const int qs = j % A8_NQ;
-      mbar_wait(&q_empty[qs], ((j / A8_NQ) & 1) ^ 1);
-      if (warp == 0 && lane == 0) {
-        A8_TR(j, 0);
-        Meta& m = meta[qs];
-        m.q0 = c_q0; m.nrows = c_nr; m.slot = c_sl; m.h = c_h; m.qt = c_qt; m.done = 0;
-        mbar_expect_tx(&q_full[qs], A8_QTX);
-        tma_2d(sQ(qs), &tmQ, c_h * 64, c_q0, &q_full[qs]);
-        tma_2d(sQ(qs) + 8192, &tmKV, c_h * 64, c_sl * T, &q_full[qs]);       // k_cls
-        tma_2d(sQ(qs) + 8320, &tmKV, D + c_h * 64, c_sl * T, &q_full[qs]);   // v_cls
+      int* rb = nullptr;
+#pragma unroll 1
+      for (int e = 0; e < HP; ++e) {        // items j, (j + 1): heads c_h, (c_h + 1)
+        const int je = j + e, he = c_h + e;
+        const int qs = je % A8_NQ;
+        mbar_wait(&q_empty[qs], ((je / A8_NQ) & 1) ^ 1);
+        if (warp == 0 && lane == 0) {
+          A8_TR(je, 0);
+          Meta& m = meta[qs];
+          m.q0 = c_q0; m.nrows = c_nr; m.slot = c_sl; m.h = he; m.qt = c_qt; m.done = 0;
+          mbar_expect_tx(&q_full[qs], A8_QTX);
+          tma_2d(sQ(qs), &tmQ, he * 64, c_q0, &q_full[qs]);
+          tma_2d(sQ(qs) + 8192, &tmKV, he * 64, c_sl * T, &q_full[qs]);       // k_cls
+          tma_2d(sQ(qs) + 8320, &tmKV, D + he * 64, c_sl * T, &q_full[qs]);   // v_cls
+        }
+        if (e == 0) {   // the pair shares its frame's rows: the first item's table serves both
+          rb = rowsbuf + qs * A8_MAXK;
+          *reinterpret_cast<int4*>(rb + 128 * half + 4 * lane) = make_int4(rows[0], rows[1], rows[2], rows[3]);
+          __syncwarp();
+        }
+        issue_tile(he * 64, rb, false);                                      // K(je)
+        if (warp == 0 && lane == 0) A8_TR(je, 1);
+        if (!A8_PAIR_PV) issue_tile(D + he * 64, rb, true);                  // V(je)
       }
-      int* rb = rowsbuf + qs * A8_MAXK;
-      *reinterpret_cast<int4*>(rb + 128 * half + 4 * lane) = make_int4(rows[0], rows[1], rows[2], rows[3]);
-      __syncwarp();
-      issue_tile(c_h * 64, rb, false);                                       // K(j)
-      if (warp == 0 && lane == 0) A8_TR(j, 1);
-      issue_tile(D + c_h * 64, rb, true);                                    // V(j)
+      if (A8_PAIR_PV) {                       // V(j), V(j + 1) into adjacent slots
+        issue_tile(D + c_h * 64, rb, true);
+        issue_tile(D + (c_h + 1) * 64, rb, true);
+      }
       if (warp == 0 && lane == 0) A8_TR(j, 2);
 #pragma unroll
       for (int i = 0; i < 4; ++i) rows[i] = nrows_[i];
       c_q0 = n_q0; c_nr = n_nr; c_sl = n_sl; c_h = n_h; c_qt = n_qt;
       have = nhave;
-      ++j;
+      j += HP;
     }
     // end markers in the next two Q slots: each softmax group waits only on its own items
     if (warp == 0)
@@ -423,6 +447,9 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       // Polling issuer: S(js) as soon as its Q, K tile and TMEM region are ready, P V(jp) as
       // soon as its P and V tile are ready, so neither waits behind the other's inputs.
       const uint32_t id_s = idesc64(256, 0), id_o = idesc64(64, 1);
+      const uint32_t id_o2 = idesc64(128, 1, 128);   // pair P V: M = 128, N = 128 (A8_PAIR_PV)
+      (void)id_o;
+      (void)id_o2;
       uint32_t kseq = 0, vseq = 0;
       int js = 0, jp = 0, j_end = 0x7fffffff;
       while (jp < j_end) {
@@ -451,6 +478,29 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
             }
           }
         }
+#if A8_PAIR_PV
+        if (jp + 1 < js) {
+          const uint32_t vs = A8_NKT + vseq % A8_NVT;   // V(jp) at slot vs, V(jp + 1) at vs + 1
+          if (mbar_test(&p_full[jp & 3], (jp >> 2) & 1) && mbar_test(&p_full[(jp + 1) & 3], ((jp + 1) >> 2) & 1) &&
+              mbar_test(&t_full[vs], (vseq / A8_NVT) & 1) && mbar_test(&t_full[vs + 1], (vseq / A8_NVT) & 1)) {
+            A8_TR(jp, 5);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_after();
+            const uint32_t reg = region(tmem, jp);   // lane half 0: M = 128 spans both items' rows
+#pragma unroll 4
+            for (int k = 0; k < A8_MAXK / 16; ++k)
+              mma_ts(reg + A8_O_OFF, reg + (uint32_t)(k * 8), sdesc_lbo(sT(vs) + (uint32_t)k * 2048, A8_TILE), id_o2,
+                     k != 0);
+            mma_commit(&t_empty[vs]);
+            mma_commit(&t_empty[vs + 1]);
+            mma_commit(&o_full[jp & 3]);
+            mma_commit(&o_full[(jp + 1) & 3]);
+            A8_TR(jp, 6);
+            vseq += 2;
+            jp += 2;
+          }
+        }
+#else
         if (jp < js) {
           const uint32_t vs = A8_NKT + vseq % A8_NVT;
           if (mbar_test(&p_full[jp & 3], (jp >> 2) & 1) && mbar_test(&t_full[vs], (vseq / A8_NVT) & 1)) {
@@ -468,6 +518,7 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
             ++jp;
           }
         }
+#endif
 #if A8_POLL_SLEEP > 0
         // nothing issuable: back off so the polling does not steal issue slots from the softmax
         // warps sharing this SM sub-partition
@@ -595,7 +646,8 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       tc_after();
       if (act) {
         float o[32];
-        tld32h<32>(reg + A8_O_OFF, o);
+        // pair P V: item j + 1 (odd) takes head h + 1's columns of the shared accumulator
+        tld32h<32>(reg + A8_O_OFF + (A8_PAIR_PV ? (uint32_t)((j & 1) * 64) : 0u), o);
         tld_wait();
         if (row < m.nrows) {
           const float il = 1.f / l;

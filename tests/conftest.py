@@ -10,6 +10,11 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+if os.environ.get("RV_LIB"):   # experiment builds (build.build_variant) under the same tests
+    from paper_2506_14107_b200 import _lib as _rv_lib
+    _rv_lib.load_library(os.environ["RV_LIB"])
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 GPU")
 
