@@ -334,6 +334,9 @@ def main():
     import synth
     from paper_2506_14107_b200 import ReuseViT, plan_gop
     from paper_2506_14107_b200.dist import shard_frames as shard
+    if os.environ.get("RV_LIB"):   # experiment builds (paper_2506_14107_b200.build.build_variant)
+        from paper_2506_14107_b200 import _lib
+        _lib.load_library(os.environ["RV_LIB"])
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -84,8 +84,15 @@ __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restri
   }
 }
 
+// RV_LN_MINB: resident CTAs per SM the register allocation must allow (ptxas gave 125 registers
+// without a bound: 2 CTAs = 16 warps per SM, 25% occupancy in ncu).  Bench at 7,200 frames
+// (gather_ln1 / ln2 ms per step): no bound 15.2 / 14.1, 3 -> 14.2 / 13.7, 4 -> 16.9 / 16.7
+// (64 registers spill the 32-value row), 1 -> 22.5 / 20.3
+#ifndef RV_LN_MINB
+#define RV_LN_MINB 3
+#endif
 template <int VPL>
-__global__ void gather_ln_kernel(const float* __restrict__ src, const int* __restrict__ rows,
+__global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_kernel(const float* __restrict__ src, const int* __restrict__ rows,
                                  const int* __restrict__ count, int M_host, const float* __restrict__ g,
                                  const float* __restrict__ b, bf16* __restrict__ dst, int D) {
   const int M = count ? *count : M_host;
