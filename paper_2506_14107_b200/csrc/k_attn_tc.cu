@@ -245,8 +245,21 @@ RV_DEV float2 exp2_poly2(unsigned long long x2) {
   return make_float2(__int_as_float((__float_as_int(tv.x) << 23) + __float_as_int(pv.x)),
                      __int_as_float((__float_as_int(tv.y) << 23) + __float_as_int(pv.y)));
 }
+// A8_L2_PREFETCH (experiment knob): L2 fetch size hint of the K/V gathers.  Bench at 7,200
+// frames: attention 83.5 ms (none), 82.4 (256 B), 82.6 (128 B): within run-to-run noise.
+#ifndef A8_L2_PREFETCH
+#define A8_L2_PREFETCH 0
+#endif
 RV_DEV void cp_async16(uint32_t dst, const void* src) {
+#if A8_L2_PREFETCH == 256
+  // L2 fetches the 256 B block: the row's K (or V) of the paired head h ^ 1, which a
+  // neighbouring CTA gathers at about the same time (item slots walk the heads fastest)
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#elif A8_L2_PREFETCH == 128
+  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
 }
 // TMEM address of region j % 4: lane half (j & 1) -> lane offset 16, column half (j >> 1) & 1
 RV_DEV uint32_t region(uint32_t tmem, int j) {
