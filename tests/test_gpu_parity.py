@@ -291,3 +291,33 @@ def test_fused_score_r1_bitwise_equal(cuda_ok, cfgname, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("cfgname,n", [("l14", 1), ("l14", 2), ("b16", 3), ("b16", 21), ("b16", 22), ("l14", 40)])
+def test_edge_video_lengths_parity(cuda_ok, cfgname, n):
+    """Degenerate and ragged schedules: a single I frame, I + one B/P, a group of 20 plus its
+    right-edge I (21), one frame into the next group (22), a group without its right edge (40):
+    every frame against the fp64 oracle, same tolerances as test_embed_parity."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, n, 0.25, seed=300 + n)
+    plan = oracle.plan_gop(n)
+    Z, M, _, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda())
+    torch.cuda.synchronize()
+    frames = list(range(n))
+    ref = oracle.reuse_embed(cfg, W, G, x, c, plan, frames=frames)
+    err, cos = metrics(Z.cpu().numpy(), ref["Z"])
+    agree, _ = mask_agreement(M.cpu().numpy(), ref, frames)
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and agree >= 0.999, (err.max(), cos.min(), agree)
+    if n == 1:
+        assert M.cpu().numpy().sum() == 0 and st["reuse_all"] == 0.0
+
+
+def test_empty_and_bad_inputs_fail_loudly(cuda_ok):
+    """n = 0 frames and mismatched codec shapes are contract errors, not silent no-ops."""
+    from paper_2506_14107_b200._lib import ReuseViTError
+    cfg = synth.CONFIGS["tiny"]
+    m, _, _ = build(cfg)
+    x, c = synth.make_video(cfg, 4, 0.3, seed=1)
+    with pytest.raises((ReuseViTError, ValueError)):
+        m.embed(torch.from_numpy(x[:0]).cuda(), torch.from_numpy(c[:0]).cuda())
