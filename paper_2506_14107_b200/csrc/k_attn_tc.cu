@@ -3,7 +3,8 @@
 // tokens; P:336 CLS attention row = feature t).  d_h = 64 and T - 1 <= 256 patch keys (CLIP
 // B/16, L/14 at 224 px); the mma.sync kernel of k_attn.cu covers the other shapes.
 //
-// Work item = (frame of the wave, head, 64-row query tile); ~47-57 of a frame's 257 queries
+// Work item = (frame of the wave, head, 64-row query tile), a CTA taking whole frame-heads and
+// running their tiles back to back on one K / V gather (A8_KV_SHARE); ~47-57 of a frame's 257 queries
 // are recomputed at the paper's reuse rates, so the MMA M is 64 (accumulator rows on lanes
 // 0-15 or 16-31 of each TMEM lane quarter).  Per item the kernel gathers 66 KB of K/V (rows
 // scattered through `kvsrc`) for ~2 MFLOP, so it is built to keep bytes in flight and to
@@ -61,6 +62,14 @@ constexpr int A8_NT = A8_NKT + A8_NVT;
 #define A8_PAIR_PV 0
 #endif
 static_assert(!A8_PAIR_PV || A8_NVT_SLOTS % 2 == 0, "pair P V needs an even V ring");
+// A8_KV_SHARE: a CTA takes whole frame-heads and runs all of their query tiles back to back on
+// one K / V gather (frames with > 64 recomputed queries, e.g. I frames with 257 = 5 tiles,
+// otherwise re-gather the same 64 KB per tile); the tiles stay in their ring slots until the
+// frame-head's last tile has used them
+#ifndef A8_KV_SHARE
+#define A8_KV_SHARE 1
+#endif
+static_assert(!(A8_KV_SHARE && A8_PAIR_PV), "A8_KV_SHARE and A8_PAIR_PV are exclusive");
 constexpr int A8_NQ = A8_NQ_SLOTS;             // Q ring slots (items the loader may run ahead)
 constexpr uint32_t A8_TILE = A8_MAXK * 128;    // 256 keys x 128 B
 // Q tile, then the CLS key's K row at +8192 (row 0 of a 1 KB swizzle atom: unswizzled) and its
@@ -84,7 +93,7 @@ constexpr uint32_t A8_O_OFF = 128;
 
 struct Meta {   // item descriptor written by loader warp 0, read by the MMA issuer and softmax
   int q0, nrows, slot, h, qt, done;
-  int pad[2];
+  int kv_first, kv_last;   // first / last query tile on this K / V gather (A8_KV_SHARE)
 };
 
 RV_DEV uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
     // slots (tile 0 of every frame-head) are all live; later tiles exist for large frames only.
     constexpr int HP = A8_PAIR_PV ? 2 : 1;        // heads per item slot
     const int Hs = H / HP;
-    const long long n_items = (long long)n_w * Hs * A8_MAX_TILES;
+    const long long n_items = (long long)n_w * Hs * (A8_KV_SHARE ? 1 : A8_MAX_TILES);
     const long long per_t = (long long)n_w * Hs;
     const long long ld = 2LL * D;
     const int half = warp;          // this warp gathers patch keys [128 half, 128 half + 128)
@@ -347,7 +356,8 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
           const int a = __ldg(qoff + w), nq = __ldg(qoff + w + 1) - a;
           live = b_qt * A8_QROWS < nq;
           b_q0 = a + b_qt * A8_QROWS;
-          b_nr = min(A8_QROWS, nq - b_qt * A8_QROWS);
+          // A8_KV_SHARE: the whole frame-head (all nq queries); otherwise one 64-row tile
+          b_nr = A8_KV_SHARE ? nq : min(A8_QROWS, nq - b_qt * A8_QROWS);
           b_sl = __ldg(&wdesc[w].x);
         }
         ball = __ballot_sync(0xffffffffu, live);
@@ -408,6 +418,34 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       int n_q0 = 0, n_nr = 0, n_sl = 0, n_h = 0, n_qt = 0, nrows_[4];
       const bool nhave = next_item(n_q0, n_nr, n_sl, n_h, n_qt);
       if (nhave) load_rows(n_sl, nrows_);
+#if A8_KV_SHARE
+      const int ntile = (c_nr + A8_QROWS - 1) / A8_QROWS;
+#pragma unroll 1
+      for (int qt = 0; qt < ntile; ++qt) {   // the frame-head's query tiles on one K / V gather
+        const int je = j + qt;
+        const int qs = je % A8_NQ;
+        mbar_wait(&q_empty[qs], ((je / A8_NQ) & 1) ^ 1);
+        if (warp == 0 && lane == 0) {
+          A8_TR(je, 0);
+          Meta& m = meta[qs];
+          m.q0 = c_q0 + qt * A8_QROWS; m.nrows = min(A8_QROWS, c_nr - qt * A8_QROWS); m.slot = c_sl; m.h = c_h;
+          m.qt = qt; m.done = 0; m.kv_first = qt == 0; m.kv_last = qt == ntile - 1;
+          mbar_expect_tx(&q_full[qs], A8_QTX);
+          tma_2d(sQ(qs), &tmQ, c_h * 64, m.q0, &q_full[qs]);
+          tma_2d(sQ(qs) + 8192, &tmKV, c_h * 64, c_sl * T, &q_full[qs]);       // k_cls
+          tma_2d(sQ(qs) + 8320, &tmKV, D + c_h * 64, c_sl * T, &q_full[qs]);   // v_cls
+        }
+        if (qt == 0) {
+          int* rb = rowsbuf + qs * A8_MAXK;
+          *reinterpret_cast<int4*>(rb + 128 * half + 4 * lane) = make_int4(rows[0], rows[1], rows[2], rows[3]);
+          __syncwarp();
+          issue_tile(c_h * 64, rb, false);                                   // K(frame-head)
+          if (warp == 0 && lane == 0) A8_TR(je, 1);
+          issue_tile(D + c_h * 64, rb, true);                                // V(frame-head)
+          if (warp == 0 && lane == 0) A8_TR(je, 2);
+        }
+      }
+#else
       int* rb = nullptr;
 #pragma unroll 1
       for (int e = 0; e < HP; ++e) {        // items j, (j + 1): heads c_h, (c_h + 1)
@@ -437,11 +475,16 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
         issue_tile(D + (c_h + 1) * 64, rb, true);
       }
       if (warp == 0 && lane == 0) A8_TR(j, 2);
+#endif
 #pragma unroll
       for (int i = 0; i < 4; ++i) rows[i] = nrows_[i];
       c_q0 = n_q0; c_nr = n_nr; c_sl = n_sl; c_h = n_h; c_qt = n_qt;
       have = nhave;
+#if A8_KV_SHARE
+      j += ntile;
+#else
       j += HP;
+#endif
     }
     // end markers in the next two Q slots: each softmax group waits only on its own items
     if (warp == 0)
@@ -475,7 +518,8 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
               continue;
             }
             const uint32_t ks = kseq % A8_NKT;
-            if (mbar_test(&r_free[js & 3], ((js >> 2) & 1) ^ 1) && mbar_test(&t_full[ks], (kseq / A8_NKT) & 1)) {
+            const bool kf = !A8_KV_SHARE || meta[qs].kv_first, kl = !A8_KV_SHARE || meta[qs].kv_last;
+            if (mbar_test(&r_free[js & 3], ((js >> 2) & 1) ^ 1) && (!kf || mbar_test(&t_full[ks], (kseq / A8_NKT) & 1))) {
               A8_TR(js, 3);
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
               tc_after();
@@ -483,10 +527,12 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
 #pragma unroll
               for (int k = 0; k < 4; ++k)   // S = Q K^T over all 256 patch keys, 16 d_h per step
                 mma_ss(reg, sdesc(sQ(qs) + k * 32), sdesc(sT(ks) + k * 32), id_s, k != 0);
-              mma_commit(&t_empty[ks]);
+              if (kl) {                      // the K tile's last user: release the slot
+                mma_commit(&t_empty[ks]);
+                ++kseq;
+              }
               mma_commit(&s_full[js & 3]);
               A8_TR(js, 4);
-              ++kseq;
               ++js;
             }
           }
@@ -516,7 +562,9 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
 #else
         if (jp < js) {
           const uint32_t vs = A8_NKT + vseq % A8_NVT;
-          if (mbar_test(&p_full[jp & 3], (jp >> 2) & 1) && mbar_test(&t_full[vs], (vseq / A8_NVT) & 1)) {
+          const int qsp = jp % A8_NQ;   // the item's Q slot (and meta) live until its epilogue
+          const bool vf = !A8_KV_SHARE || meta[qsp].kv_first, vl = !A8_KV_SHARE || meta[qsp].kv_last;
+          if (mbar_test(&p_full[jp & 3], (jp >> 2) & 1) && (!vf || mbar_test(&t_full[vs], (vseq / A8_NVT) & 1))) {
             A8_TR(jp, 5);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_after();
@@ -524,10 +572,12 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
 #pragma unroll 4
             for (int k = 0; k < A8_MAXK / 16; ++k)   // O = P V: 16 keys per MMA, P packed columns 8 k
               mma_ts(reg + A8_O_OFF, reg + (uint32_t)(k * 8), sdesc(sT(vs) + (uint32_t)k * 2048), id_o, k != 0);
-            mma_commit(&t_empty[vs]);
+            if (vl) {                        // the V tile's last user: release the slot
+              mma_commit(&t_empty[vs]);
+              ++vseq;
+            }
             mma_commit(&o_full[jp & 3]);
             A8_TR(jp, 6);
-            ++vseq;
             ++jp;
           }
         }

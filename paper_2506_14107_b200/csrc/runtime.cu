@@ -1174,13 +1174,21 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
   std::vector<int> log((size_t)ctx->L * nwv * 2);
   CK(cudaMemcpy(log.data(), ctx->count_log, log.size() * sizeof(int), cudaMemcpyDeviceToHost));
   const double D = ctx->D, T = ctx->T, N = ctx->N, F = ctx->F, Hr = ctx->Hr, n = ctx->cur_n;
-  // per-wave host facts: frames, decision frames and their reference rows
+  // per-wave host facts: frames, decision frames and the DISTINCT reference frames they read
+  // (compulsory traffic: a reference shared by several frames of the wave counts once)
   std::vector<double> wdec(nwv, 0), wrefs(nwv, 0);
+  std::vector<int> ref_seen((size_t)std::max(ctx->n_cap, 1), -1);
   for (int wi = 0; wi < nwv; ++wi) {
     const Wave& wv = ctx->waves[wi];
     for (int j = 0; j < wv.n_w; ++j) {
       const int* d = &ctx->wdesc_host[(size_t)(wv.off + j) * 4];
-      if (d[3] != RV_I) { wdec[wi] += 1; wrefs[wi] += (d[1] >= 0) + (d[2] >= 0); }
+      if (d[3] == RV_I) continue;
+      wdec[wi] += 1;
+      for (int k = 1; k <= 2; ++k)
+        if (d[k] >= 0 && d[k] < (int)ref_seen.size() && ref_seen[d[k]] != wi) {
+          ref_seen[d[k]] = wi;
+          wrefs[wi] += 1;
+        }
     }
   }
   std::vector<rv_kernel_prof> acc(K_NCLS);
