@@ -24,8 +24,14 @@ constexpr int SCORE_TOK = 32;      // tokens per CTA (8 warps x 4 tokens): grid 
 // VPL > 0: D == 128 * VPL, the token's 3 x VPL float4 per lane are loaded unconditionally
 // (a missing reference re-reads the current row, an L1 hit) and without a loop-carried branch,
 // so all of them are in flight together; VPL == 0: generic D.
+// RV_SCORE_MINB: resident CTAs per SM for the register allocation.  Bench at 7,200 frames (score
+// ms per step): no bound (ptxas: 64 registers) 83.8; 3 (80 registers) 78.8; 2 (128) 87.7;
+// 1 (unbounded) 127
+#ifndef RV_SCORE_MINB
+#define RV_SCORE_MINB 3
+#endif
 template <int VPL>
-__global__ void __launch_bounds__(SCORE_THREADS)
+__global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
     score_kernel(const float* __restrict__ X, int T, int D, int N, int L, int layer,
                  const int4* __restrict__ wdesc, const float* __restrict__ tsrc, int tH,
                  const float* __restrict__ codec, const uint8_t* force,
