@@ -19,7 +19,12 @@ namespace rv {
 namespace {
 
 constexpr int SCORE_THREADS = 256;
-constexpr int SCORE_TOK = 32;      // tokens per CTA (8 warps x 4 tokens): grid = n_w x ceil(N/32)
+// tokens per CTA (8 warps x 8 tokens): grid = n_w x ceil(N / 64).  Bench at 7,200 frames (score
+// ms per step, 3 CTAs per SM): 16 -> 83.8, 32 -> 79.1, 64 -> 77.1-77.4, 128 -> 79.3, 256 -> 84.7
+#ifndef RV_SCORE_TOK
+#define RV_SCORE_TOK 64
+#endif
+constexpr int SCORE_TOK = RV_SCORE_TOK;
 
 // VPL > 0: D == 128 * VPL, the token's 3 x VPL float4 per lane are loaded unconditionally
 // (a missing reference re-reads the current row, an L1 hit) and without a loop-carried branch,
