@@ -597,9 +597,14 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   // (17 -> 20 ms as pairs: half as many 256-row tiles on small waves)
   static const int pair_on = getenv("RV_GEMM_PAIR") ? atoi(getenv("RV_GEMM_PAIR")) : 1;
   if (p.K <= 2 * BK && e.resid) return launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
+// RV_GEMM_RE_KMAX: largest K that takes the 16-warp epilogue (MODE 2).  FC2 (K = 4096) as MODE 2
+// pairs: 70.1 vs 60.8 ms per step as MODE 0 pairs (fewer stages for its long mainloop)
+#ifndef RV_GEMM_RE_KMAX
+#define RV_GEMM_RE_KMAX 1024
+#endif
   if constexpr (BN == 256) {
     if (pair_on) {
-      if (re_on && p.K <= 1024 && (e.resid ? BN >= 128 : BN == 256))
+      if (re_on && p.K <= RV_GEMM_RE_KMAX && (e.resid ? BN >= 128 : BN == 256))
         return launch_pair<BN, 2>(p, M_dev, M_host, max_m, e, s);
       return launch_pair<BN, 0>(p, M_dev, M_host, max_m, e, s);
     }
