@@ -136,8 +136,29 @@ int grid_rows(long long rows) {
 
 }  // namespace
 
+// one warp per patch row, float4 loads and 8 B bf16 stores (pp % 4 == 0), zero padding to KP
+__global__ void __launch_bounds__(256) patch_to_bf16_rows_kernel(const float* __restrict__ src, bf16* __restrict__ dst,
+                                                                 long long rows, int pp, int KP) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + r * pp);
+    uint2* d2 = reinterpret_cast<uint2*>(dst + r * KP);
+    for (int c = lane; c < KP / 4; c += 32) {
+      const float4 v = c < pp / 4 ? __ldg(s4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      d2[c] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    }
+  }
+}
+
 cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP,
                                  cudaStream_t s) {
+  if (pp % 4 == 0 && KP % 4 == 0) {   // vectorised path (all CLIP shapes: pp = 3 p^2 with even p)
+    long long g = (rows + 7) / 8;
+    if (g > 148 * 16) g = 148 * 16;
+    patch_to_bf16_rows_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(src, dst, rows, pp, KP);
+    return cudaGetLastError();
+  }
   long long total = rows * KP;
   long long g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
