@@ -333,6 +333,8 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   // override for experiments.
   const int bn_resid = getenv("RV_BN_RESID") ? atoi(getenv("RV_BN_RESID")) : 256;
   const int bn_r2 = getenv("RV_BN_R2") ? atoi(getenv("RV_BN_R2")) : 256;
+  // measured at 7,200 frames: RV_BN_R1=64 -> R1 17.7 -> 28.9 ms, RV_BN_R2=128 -> R2 60.4 -> 71.1
+  const int bn_r1 = getenv("RV_BN_R1") ? atoi(getenv("RV_BN_R1")) : 256;
   ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
   ctx->g_r1.resize(L); ctx->g_r2.resize(L); ctx->g_r2f.resize(L); ctx->tm_wr1.resize(L);
   // RV_SCORE_R1=1: fused score + R1 (k_score_r1.cu).  Off by default: correct (the whole -m gpu
@@ -347,7 +349,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
               gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
               gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e, bn_resid);
     if (ok && ctx->gates_loaded)
-      ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
+      ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e, bn_r1) &&
            gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
     if (ok && ctx->fuse_r1)
       ok = make_tmap_bf16(&ctx->tm_wr1[l], w.Wr1, ctx->Hr, (int)D, ctx->Hr, e, sizeof e) &&
