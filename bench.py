@@ -229,7 +229,7 @@ def run_c5(args):
 
     import synth
     from paper_2506_14107_b200 import ReuseViT, plan_gop
-    from paper_2506_14107_b200.dist import combine_plans, lpt_assign, reuse_estimate
+    from paper_2506_14107_b200.dist import combine_plans, gather_rows, lpt_assign, max_over_ranks, reuse_estimate
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -263,16 +263,13 @@ def run_c5(args):
     emb = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
     masks = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    n_max = max(len(a) for a in assign) * args.video_frames
-    zp = torch.zeros((n_max, D), dtype=torch.float32, device=dev)
-    zg = torch.empty((world * n_max, D), dtype=torch.float32, device=dev)
+    counts = [len(a) * args.video_frames for a in assign]
 
     def step():
         m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream)
         st = m.wait()
         if world > 1:
-            zp[:n_loc] = emb
-            dist.all_gather_into_tensor(zg, zp)
+            gather_rows([emb], counts)
         return st
 
     for _ in range(args.warmup):
@@ -293,10 +290,7 @@ def run_c5(args):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     loads = [sum(costs[v] for v in a) for a in assign]
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms)
     n_total = args.videos * args.video_frames
     line = {"metric": "ViT-L/14@336 ReuseViT multi-video embedding frames/sec (64 videos x 120 frames)",
             "value": n_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -333,7 +327,7 @@ def main():
 
     import synth
     from paper_2506_14107_b200 import ReuseViT, plan_gop
-    from paper_2506_14107_b200.dist import shard_frames as shard
+    from paper_2506_14107_b200.dist import gather_rows, max_over_ranks, shard_frames as shard
     if os.environ.get("RV_LIB"):   # experiment builds (paper_2506_14107_b200.build.build_variant)
         from paper_2506_14107_b200 import _lib
         _lib.load_library(os.environ["RV_LIB"])
@@ -367,22 +361,14 @@ def main():
     emb = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
     masks = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    n_max = max(shard(n_total, args.refresh, r, world)[2] for r in range(world))
-    if world > 1:
-        g_emb = torch.empty((world * n_max, D), dtype=torch.float32, device=dev)
-        g_msk = torch.empty((world * n_max, L * N), dtype=torch.uint8, device=dev)
-        p_emb = torch.zeros((n_max, D), dtype=torch.float32, device=dev)
-        p_msk = torch.zeros((n_max, L * N), dtype=torch.uint8, device=dev)
+    counts = [shard(n_total, args.refresh, r, world)[1] for r in range(world)]
 
     def step(profile):
         m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync,
                       chain=args.chain)
         st = m.wait()
-        if world > 1:     # NCCL over NVLink only to gather embeddings + masks (SURVEY D9)
-            p_emb[:n_loc].copy_(emb)
-            p_msk[:n_loc].copy_(masks.view(n_loc, -1))
-            dist.all_gather_into_tensor(g_emb, p_emb)
-            dist.all_gather_into_tensor(g_msk, p_msk)
+        if world > 1:     # NCCL over NVLink only to gather embeddings + masks (SURVEY D9, a15)
+            gather_rows([emb, masks.view(n_loc, -1)], counts)
         return st
 
     for _ in range(max(args.warmup, 1)):
@@ -409,10 +395,7 @@ def main():
     waves_info = {"frames_per_wave": wc["frames"].tolist(),
                   "M_C_mean_over_layers": [round(float(v), 1) for v in wc["M_C"].mean(axis=0)],
                   "M_R_mean_over_layers": [round(float(v), 1) for v in wc["M_R"].mean(axis=0)]}
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms)
     value = n_total / (ms / 1e3)       # emitted frames only; halo frames cost time, not count
 
     # ---- e2e through the public API with host buffers (pinned), H2D/D2H inside the step.
@@ -432,12 +415,7 @@ def main():
         h2d = int(xh.numel() * 4 + ch.numel() * 4)
         d2h = int(outs[0].size * 4 + outs[1].size)
 
-        def max_ranks(v):
-            if world > 1:
-                t = torch.tensor([v], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                v = float(t.item())
-            return v
+        max_ranks = max_over_ranks
 
         def hstep():
             m.embed_async(xh.numpy(), ch.numpy(), plan, out=outs, stream=stream)

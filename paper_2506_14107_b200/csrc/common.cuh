@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define RV_DEV __device__ __forceinline__
 
 namespace rv {
@@ -44,6 +46,38 @@ RV_DEV uint32_t pack_bf16x2(float lo, float hi) {
 RV_DEV float2 unpack_bf16x2(uint32_t u) {
   __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
   return __bfloat1622float2(h);
+}
+
+// ---- per-device host caches.  Function attributes and SM counts belong to a device, and one
+// process may drive several GPUs through one library instance: cache per device, thread-safe.
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : (d & 63);
+}
+inline int dev_sms() {
+  static std::atomic<int> cache[64];
+  const int d = cur_device();
+  int n = cache[d].load(std::memory_order_relaxed);
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+    cache[d].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+// Raise kernel Kern's dynamic shared-memory limit to >= smem bytes on the current device.
+template <auto Kern>
+cudaError_t ensure_smem(size_t smem) {
+  static std::atomic<size_t> done[64];
+  const int d = cur_device();
+  if (done[d].load() >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  size_t cur = done[d].load();
+  while (cur < smem && !done[d].compare_exchange_weak(cur, smem)) {
+  }
+  return cudaSuccess;
 }
 
 }  // namespace rv

@@ -260,12 +260,8 @@ cudaError_t launch_attn_dh(const bf16* q, const bf16* KV, const int* kvsrc, bf16
                            cudaStream_t s) {
   const int Tp = (T + 15) / 16 * 16;
   const size_t smem = (size_t)(4 * KB * (DH + 8) + QT * (DH + 8)) * sizeof(bf16) + (size_t)Tp * 8;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  cudaError_t e = ensure_smem<attn_kernel<DH>>(smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(H, n_w);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   attn_kernel<DH><<<grid, 128, smem, s>>>(q, KV, kvsrc, out, reinterpret_cast<const int4*>(wdesc), qoff, pclsh, T,

@@ -792,19 +792,9 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV,
   if (n_w <= 0) return cudaSuccess;
   if (!attn_tc_supported(T, D, H)) return cudaErrorInvalidValue;
   const size_t smem = attn_tc_smem();
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  cudaError_t e = ensure_smem<attn_tc_kernel>(smem);
+  if (e != cudaSuccess) return e;
+  const int sms = dev_sms();
   const long long items = (long long)n_w * H;   // tile-0 items (all live)
   const int grid = items < sms ? (int)items : sms;
   const float scale_log2 = 1.4426950408889634f / 8.0f;   // 1/sqrt(64) * log2(e)

@@ -513,27 +513,13 @@ bool encode_2d(CUtensorMap* m, const void* ptr, long long rows, int cols, int bo
   return true;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return dev_sms(); }
 
 template <int BN, int MODE>
 cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
   using C = Cfg<BN, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           C::SMEM);
-    if (err != cudaSuccess) return err;
-    attr = true;
-  }
+  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, false>>(C::SMEM);
+  if (err != cudaSuccess) return err;
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
@@ -545,13 +531,8 @@ cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max
 template <int BN, int MODE>
 cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
   using C = Cfg<BN, MODE, true>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           C::SMEM);
-    if (err != cudaSuccess) return err;
-    attr = true;
-  }
+  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, true>>(C::SMEM);
+  if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(gemm_threads<BN, MODE>());
   cfg.dynamicSmemBytes = C::SMEM;
@@ -565,7 +546,8 @@ cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max
   cfg.numAttrs = 1;
   // persistent: only as many pairs as can be co-resident (TPC pairing can leave SMs unpaired;
   // a second wave of pairs would double the time of the tiles they own)
-  static int max_pairs = 0;
+  static std::atomic<int> max_pairs_dev[64];   // per device (cudaOccupancyMaxActiveClusters)
+  int max_pairs = max_pairs_dev[cur_device()].load();
   if (!max_pairs) {
     cfg.gridDim = dim3(num_sms() & ~1);
     int n = 0;
@@ -574,7 +556,7 @@ cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max
       n = num_sms() / 2;
     }
     max_pairs = n < num_sms() / 2 ? n : num_sms() / 2;
-    if (getenv("RV_GEMM_DEBUG")) fprintf(stderr, "[gemm] BN=%d MODE=%d: %d co-resident CTA pairs\n", BN, MODE, n);
+    max_pairs_dev[cur_device()].store(max_pairs);
   }
   const int tiles = ((max_m + C::TILE_M - 1) / C::TILE_M) * (p.N / BN);
   int pairs = max_pairs;
@@ -584,18 +566,25 @@ cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE, true>, p.tmA, p.tmB2, M_dev, M_host, p.N, p.K, e);
 }
 
+#ifndef RV_GEMM_RE
+#define RV_GEMM_RE 1
+#endif
+#ifndef RV_GEMM_PAIR
+#define RV_GEMM_PAIR 1
+#endif
 template <int BN>
 cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e,
                       cudaStream_t s) {
   // short K with a residual: 2-stage mainloop + cp.async residual ring (R2); a gathered residual
   // with K <= 1024 (W_o): 16 epilogue warps, 3 stages (tools/r2_bench.py: 57 -> 52 us on a
-  // 16k-row W_o; FC2's K = 4096 mainloop needs its 4 stages).  RV_GEMM_RE=0 disables.
-  static const bool re_on = !getenv("RV_GEMM_RE") || atoi(getenv("RV_GEMM_RE")) != 0;
-  // RV_GEMM_PAIR: 0 off, 1 (default) CTA pairs (256 x 256 tiles) for the MODE 0 / 2 GEMMs with
+  // 16k-row W_o; FC2's K = 4096 mainloop needs its 4 stages).  Experiment builds only
+  // (build.build_variant): -DRV_GEMM_RE=0 disables.
+  constexpr bool re_on = RV_GEMM_RE != 0;
+  // RV_GEMM_PAIR (compile-time): CTA pairs (256 x 256 tiles) for the MODE 0 / 2 GEMMs with
   // BN = 256 (tools/gemm_bench.py at M = 80k: QKV 432 -> 385 us, FC1 572 -> 521, FC2 508 -> 464,
   // W_o 193 -> 154; in the bench FC2 67 -> 60 ms per step); R1 (N = 128) stays single-CTA
   // (17 -> 20 ms as pairs: half as many 256-row tiles on small waves)
-  static const int pair_on = getenv("RV_GEMM_PAIR") ? atoi(getenv("RV_GEMM_PAIR")) : 1;
+  constexpr bool pair_on = RV_GEMM_PAIR != 0;
   if (p.K <= 2 * BK && e.resid) return launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
 // RV_GEMM_RE_KMAX: largest K that takes the 16-warp epilogue (MODE 2).  FC2 (K = 4096) as MODE 2
 // pairs: 70.1 vs 60.8 ms per step as MODE 0 pairs (fewer stages for its long mainloop)

@@ -72,13 +72,10 @@ struct rv_ctx {
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
   bf16* dfull = nullptr;      // [max_w][T][D] Delta of reused tokens (wave-local token rows, bf16)
   int* rpos = nullptr;        // [max_w][T] compact restoration row of token w*T+i (-1: recomputed)
-  // fused score + R1 (k_score_r1.cu): hr of reused tokens at their wave-local rows, and R2's
-  // per-row maps over all wave-local rows (output row or -1; the provider's row)
-  bf16* hr_full = nullptr;    // [max_w][T][Hr]
-  int *r2_out = nullptr, *r2_res = nullptr;   // [max_w][T]
-  bool fuse_r1 = false;
-  std::vector<CUtensorMap> tm_wr1;   // Wr1 [Hr][D], box {64, Hr}
   bf16* patches_bf16 = nullptr;
+  // host-pointer embeds only (no RV_DEVICE_PTRS): staging copies of the caller's host buffers
+  int h_cap = 0, hs_cap = 0;
+  std::vector<void*> hallocs, hsallocs;
   float *in_patches = nullptr, *in_codec = nullptr, *out_emb = nullptr, *out_scores = nullptr;
   uint8_t* out_masks = nullptr;
   int* wdesc = nullptr;
@@ -101,7 +98,7 @@ struct rv_ctx {
   GemmPlan pe;
   CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
   CUtensorMap tmKV;                // K/V cache [n T][2 D], box {64, 1}: row gathers (tcgen05 attention)
-  std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2, g_r2f;
+  std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
   // ---- graph cache
   cudaGraphExec_t gexec = nullptr;
   std::vector<long long> gkey;
@@ -266,21 +263,35 @@ rv_status check_plan(rv_ctx* ctx, const rv_plan* p, std::vector<int>* level_out)
 }
 
 // ------------------------------------------------------------------ buffers
+// Drop every per-embed buffer and the state encoded from their addresses (graph, tensor maps,
+// GEMM plans): after a failed re-allocation the context holds no dangling pointer, and the
+// next embed allocates again from scratch.
+void release_buffers(rv_ctx* ctx) {
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  free_list(ctx->ballocs);
+  ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0; ctx->chain_cap = 0;
+  ctx->X[0] = ctx->X[1] = nullptr; ctx->KV = nullptr; ctx->pclsh = nullptr; ctx->kvsrc = nullptr;
+  ctx->dfull = nullptr; ctx->rpos = nullptr; ctx->patches_bf16 = nullptr; ctx->wdesc = nullptr;
+  ctx->wmask = ctx->wprov = nullptr;
+  ctx->cntR = ctx->idxC = ctx->idxR = ctx->provrow = ctx->qoff = ctx->counts = nullptr;
+  ctx->A = ctx->q = ctx->att = ctx->h = ctx->hr = nullptr; ctx->x1 = nullptr; ctx->reuse_ctr = nullptr;
+  ctx->QKVc[0] = ctx->QKVc[1] = nullptr; ctx->XP = nullptr; ctx->kvsrc2 = nullptr; ctx->pcl2 = nullptr;
+  ctx->wrows = nullptr; ctx->qoffT = nullptr;
+}
+
 rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int max_w) {
   capC = (capC + 127) / 128 * 128;
   capR = std::max<long long>(128, (capR + 127) / 128 * 128);
   if (n <= ctx->n_cap && capC <= ctx->capC && capR <= ctx->capR && max_w <= ctx->wdesc_cap) return RV_OK;
-  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
-  free_list(ctx->ballocs);
-  ctx->chain_cap = 0;   // the chain-variant buffers were in the same list
   n = std::max(n, ctx->n_cap);
   capC = std::max(capC, ctx->capC);
   capR = std::max(capR, ctx->capR);
   max_w = std::max(max_w, ctx->wdesc_cap);
+  release_buffers(ctx);
   const long long T = ctx->T, D = ctx->D, N = ctx->N;
   auto& B = ctx->ballocs;
   rv_status s;
-#define AL(ptr, cnt) if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) return s
+#define AL(ptr, cnt) if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) { release_buffers(ctx); return s; }
   AL(ctx->X[0], n * T * D);
   AL(ctx->X[1], n * T * D);
   AL(ctx->KV, n * T * 2 * D);
@@ -288,15 +299,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->kvsrc, n * T);
   AL(ctx->dfull, (size_t)max_w * T * D);
   AL(ctx->rpos, max_w * T);
-  AL(ctx->hr_full, (size_t)max_w * T * ctx->Hr);
-  AL(ctx->r2_out, max_w * T);
-  AL(ctx->r2_res, max_w * T);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
-  AL(ctx->in_patches, (size_t)n * N * ctx->pp);
-  AL(ctx->in_codec, n * N);
-  AL(ctx->out_emb, n * D);
-  AL(ctx->out_masks, (size_t)n * ctx->L * N);
-  AL(ctx->out_scores, (size_t)n * ctx->L * N);
   AL(ctx->wdesc, (size_t)n * 4);
   AL(ctx->wmask, max_w * T);
   AL(ctx->wprov, max_w * T);
@@ -314,47 +317,61 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->hr, capR * ctx->Hr);
   AL(ctx->reuse_ctr, 64);
 #undef AL
-  // the restoration GEMMs also read the never-written Delta rows of C tokens (results discarded)
-  if (cudaMemset(ctx->dfull, 0, (size_t)max_w * T * D * sizeof(bf16)) != cudaSuccess ||
-      cudaMemset(ctx->hr_full, 0, (size_t)max_w * T * ctx->Hr * sizeof(bf16)) != cudaSuccess)
+  // the restoration GEMM R1 also reads the never-written Delta rows of C tokens (results discarded)
+  if (cudaMemset(ctx->dfull, 0, (size_t)max_w * T * D * sizeof(bf16)) != cudaSuccess) {
+    release_buffers(ctx);
     return fail(ctx, RV_ECUDA, "cudaMemset failed");
+  }
+  char e[256];
+  bool ok = make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 64, e, sizeof e) &&
+            make_tmap_bf16(&ctx->tmKV, ctx->KV, (long long)n * T, 2 * (int)D, 1, e, sizeof e) &&
+            gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e);
+  const int L = ctx->L;
+  ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
+  ctx->g_r1.resize(L); ctx->g_r2.resize(L);
+  for (int l = 0; ok && l < L; ++l) {
+    const LayerW& w = ctx->lw[l];
+    ok = gemm_make_plan(&ctx->g_qkv[l], ctx->A, capC, w.Wqkv, 3 * (int)D, (int)D, e, sizeof e) &&
+         gemm_make_plan(&ctx->g_wo[l], ctx->att, capC, w.Wo, (int)D, (int)D, e, sizeof e) &&
+         gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
+         gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e);
+    if (ok && ctx->gates_loaded)
+      ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
+           gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e);
+  }
+  if (!ok) {
+    release_buffers(ctx);
+    return fail(ctx, RV_ECUDA, "%s", e);
+  }
   ctx->n_cap = n;
   ctx->capC = capC;
   ctx->capR = capR;
   ctx->wdesc_cap = max_w;
-  char e[256];
-  if (!make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 64, e, sizeof e) ||
-      !make_tmap_bf16(&ctx->tmKV, ctx->KV, (long long)n * T, 2 * (int)D, 1, e, sizeof e))
-    return fail(ctx, RV_ECUDA, "%s", e);
-  if (!gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e))
-    return fail(ctx, RV_ECUDA, "%s", e);
-  const int L = ctx->L;
-  // N-tile of the residual-streaming GEMMs (W_o, FC2, restoration R2); RV_BN_RESID / RV_BN_R2
-  // override for experiments.
-  const int bn_resid = getenv("RV_BN_RESID") ? atoi(getenv("RV_BN_RESID")) : 256;
-  const int bn_r2 = getenv("RV_BN_R2") ? atoi(getenv("RV_BN_R2")) : 256;
-  // measured at 7,200 frames: RV_BN_R1=64 -> R1 17.7 -> 28.9 ms, RV_BN_R2=128 -> R2 60.4 -> 71.1
-  const int bn_r1 = getenv("RV_BN_R1") ? atoi(getenv("RV_BN_R1")) : 256;
-  ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
-  ctx->g_r1.resize(L); ctx->g_r2.resize(L); ctx->g_r2f.resize(L); ctx->tm_wr1.resize(L);
-  // RV_SCORE_R1=1: fused score + R1 (k_score_r1.cu).  Off by default: correct (the whole -m gpu
-  // suite passes with it, bitwise equal outputs) but 201 ms per step vs 83 + 17 unfused -- its
-  // 128 KB A tile leaves one 16-warp CTA per SM, a quarter of the score kernel's loads in flight
-  static const bool fuse_env = getenv("RV_SCORE_R1") && atoi(getenv("RV_SCORE_R1")) != 0;
-  ctx->fuse_r1 = fuse_env && ctx->gates_loaded && score_r1_supported((int)D, ctx->Hr);
-  for (int l = 0; l < L; ++l) {
-    const LayerW& w = ctx->lw[l];
-    bool ok = gemm_make_plan(&ctx->g_qkv[l], ctx->A, capC, w.Wqkv, 3 * (int)D, (int)D, e, sizeof e) &&
-              gemm_make_plan(&ctx->g_wo[l], ctx->att, capC, w.Wo, (int)D, (int)D, e, sizeof e, bn_resid) &&
-              gemm_make_plan(&ctx->g_fc1[l], ctx->A, capC, w.W1, ctx->F, (int)D, e, sizeof e) &&
-              gemm_make_plan(&ctx->g_fc2[l], ctx->h, capC, w.W2, (int)D, ctx->F, e, sizeof e, bn_resid);
-    if (ok && ctx->gates_loaded)
-      ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e, bn_r1) &&
-           gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
-    if (ok && ctx->fuse_r1)
-      ok = make_tmap_bf16(&ctx->tm_wr1[l], w.Wr1, ctx->Hr, (int)D, ctx->Hr, e, sizeof e) &&
-           gemm_make_plan(&ctx->g_r2f[l], ctx->hr_full, max_w * T, w.Wr2, (int)D, ctx->Hr, e, sizeof e, bn_r2);
-    if (!ok) return fail(ctx, RV_ECUDA, "%s", e);
+  return RV_OK;
+}
+
+// Staging buffers of host-pointer embeds (never allocated on the RV_DEVICE_PTRS path).
+rv_status ensure_host_buffers(rv_ctx* ctx, int n, bool scores) {
+  rv_status s;
+  if (n > ctx->h_cap) {
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    free_list(ctx->hallocs);
+    ctx->h_cap = 0;
+    const long long N = ctx->N;
+#define AL(ptr, cnt) if ((s = dalloc(ctx, ctx->hallocs, &ptr, (size_t)(cnt)))) { free_list(ctx->hallocs); return s; }
+    AL(ctx->in_patches, (size_t)n * N * ctx->pp);
+    AL(ctx->in_codec, n * N);
+    AL(ctx->out_emb, (size_t)n * ctx->D);
+    AL(ctx->out_masks, (size_t)n * ctx->L * N);
+#undef AL
+    ctx->h_cap = n;
+  }
+  if (scores && n > ctx->hs_cap) {
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+    free_list(ctx->hsallocs);
+    ctx->hs_cap = 0;
+    if ((s = dalloc(ctx, ctx->hsallocs, &ctx->out_scores, (size_t)n * ctx->L * ctx->N))) return s;
+    ctx->hs_cap = n;
   }
   return RV_OK;
 }
@@ -422,19 +439,12 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       const int n_w = wv.n_w;
       const int* wd = ctx->wdesc + (size_t)wv.off * 4;
       const int maxC = n_w * T;
-      // a2-a3: Eq. 1-4 (fused with R1 of a12 when the wave restores anything)
-      const bool fused = ctx->fuse_r1 && wv.any_ref && !dense;
+      // a2-a3: Eq. 1-4
       r.begin(K_SCORE,l,wi);
-      if (fused)
-        r.chk(launch_score_r1(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr, w.gate,
-                              ctx->Hg, masks, scores, ctx->wmask, ctx->wprov, ctx->cntR, &ctx->tm_wr1[l], w.br1,
-                              ctx->hr_full, ctx->r2_out, ctx->r2_res, s),
-              "score_r1");
-      else
-        r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
-                           ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
-                           ctx->wprov, ctx->cntR, ctx->dfull, s),
-              "score");
+      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
+                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
+                         ctx->wprov, ctx->cntR, ctx->dfull, s),
+            "score");
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
@@ -511,20 +521,8 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       // a12: restoration (Eq. 9) + merge (Eq. 10, R side).  The score pass wrote Delta (Eq. 8)
       // into the wave-local token rows w*T+i; R1 reads them in place over all n_w*T rows and
       // stores only the reused rows, compacted (row map rpos; -1 for C rows): no Delta copy.
-      // R2 runs over the M_R compact rows.  Fused: R1 ran inside the score pass; R2 runs over
-      // all n_w * T wave-local rows of hr with the score pass's row maps (-1: not reused).
-      if (fused) {
-        Epi e2;
-        e2.bias = w.br2;
-        e2.resid = Xout;
-        e2.resid_rows = ctx->r2_res;
-        e2.resid_ld = D;
-        e2.out = Xout;
-        e2.out_rows = ctx->r2_out;
-        e2.out_ld = D;
-        r.begin(K_R2,l,wi);
-        r.chk(gemm_launch(ctx->g_r2f[l], nullptr, n_w * T, n_w * T, e2, s), "gemm_r2");
-      } else if (wv.any_ref && !dense) {
+      // R2 runs over the M_R compact rows.
+      if (wv.any_ref && !dense) {
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;
@@ -896,8 +894,7 @@ rv_status rv_load_vit(rv_ctx* ctx, const float* blob, size_t n_floats) {
   if ((s = upload_f(ctx, W, &ctx->lnpost_b, p, D))) return s;
   p += D;
   ctx->vit_loaded = true;
-  ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0;   // re-encode tensor maps
-  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  release_buffers(ctx);   // the GEMM plans encode the weight addresses: rebuilt at the next embed
   return RV_OK;
 }
 
@@ -923,8 +920,7 @@ rv_status rv_load_gates(rv_ctx* ctx, const float* blob, size_t n_floats) {
     if ((s = upload_f(ctx, W, &w.br2, p, D))) return s; p += D;
   }
   ctx->gates_loaded = true;
-  ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0;
-  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  release_buffers(ctx);
   return RV_OK;
 }
 
@@ -1005,11 +1001,15 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   ctx->prof_valid = false;
   cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : nullptr;
   const bool devp = flags & RV_DEVICE_PTRS;
+  if (devp && ((uintptr_t)patches & 15))
+    return fail(ctx, RV_ECONTRACT, "rv_embed: device patches must be 16-byte aligned (vectorised loads)");
+  if (!devp && (st = ensure_host_buffers(ctx, n, scores != nullptr))) return st;
   const float* d_patches = devp ? patches : ctx->in_patches;
   const float* d_codec = devp ? codec : ctx->in_codec;
   float* d_emb = devp ? emb : ctx->out_emb;
-  uint8_t* d_masks = devp ? (masks ? masks : ctx->out_masks) : ctx->out_masks;
-  float* d_scores = devp ? (scores ? scores : ctx->out_scores) : ctx->out_scores;
+  // masks / scores are written only when requested (the kernels skip null outputs)
+  uint8_t* d_masks = devp ? masks : (masks ? ctx->out_masks : nullptr);
+  float* d_scores = devp ? scores : (scores ? ctx->out_scores : nullptr);
   // Graph capture cannot run on the legacy NULL stream: work on the context's own stream,
   // ordered after / before the caller's stream with events.
   cudaStream_t ws = s ? s : ctx->own_stream;
@@ -1147,6 +1147,8 @@ void rv_destroy(rv_ctx* ctx) {
   if (ctx->inflight) cudaEventSynchronize(ctx->ev[3]);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   free_list(ctx->ballocs);
+  free_list(ctx->hallocs);
+  free_list(ctx->hsallocs);
   free_list(ctx->wallocs);
   if (ctx->count_log) cudaFree(ctx->count_log);
   for (auto e : ctx->prof_pool) cudaEventDestroy(e);

@@ -60,13 +60,6 @@ cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float
                            cudaStream_t s);
 
 // ---------------------------------------------------------------- decision + compaction (k_score.cu)
-// fused decision + first restoration layer (k_score_r1.cu): D in {768, 1024}, Hr = 128
-bool score_r1_supported(int D, int Hr);
-cudaError_t launch_score_r1(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
-                            const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
-                            int Hg, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov, int* cntR,
-                            const CUtensorMap* tmW1, const float* br1, bf16* hr_full, int* r2_out, int* r2_res,
-                            cudaStream_t s);
 cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,

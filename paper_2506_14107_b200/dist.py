@@ -28,6 +28,55 @@ def shard_frames(n_total: int, refresh: int, rank: int, world: int) -> Tuple[int
     return f0, f1 - f0, f1 - f0 + halo
 
 
+def _collective_device(group, like=None):
+    """Device the collective runs on: NCCL needs CUDA tensors even on a rank with no work."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return like.device if like is not None else torch.device("cpu")
+
+
+def gather_rows(parts, counts, group=None):
+    """All-gather per-rank row blocks of different lengths (the a15 step).
+
+    ``parts``: this rank's tensors [>= counts[rank], ...] (rows beyond counts[rank] ignored);
+    ``counts``: rows owned by every rank (known to all ranks from the sharding, so no extra
+    collective).  Each tensor is padded to max(counts) rows and gathered with ONE collective
+    (NCCL ``all_gather_into_tensor`` over NVLink; the list form on gloo).  A rank that owns no
+    rows still takes part (its padding lives on the collective's device).  Returns the valid
+    rows of all ranks concatenated in rank order, one tensor per input."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n_max = max(max(counts), 1)
+    out = []
+    for t in parts:
+        dev = _collective_device(group, t)
+        pad = torch.zeros((n_max,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+        if counts[rank]:
+            pad[:counts[rank]] = t[:counts[rank]].to(dev)
+        full = torch.empty((world * n_max,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(full, pad, group=group)
+        else:
+            dist.all_gather(list(full.chunk(world)), pad, group=group)
+        out.append(torch.cat([full[r * n_max:r * n_max + counts[r]] for r in range(world)]))
+    return out
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    """Max of a per-rank float (device-timed step times: the contract's max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_collective_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 def embed_sharded(model, patches, codec, refresh: int = 20, group=None, **embed_kw):
     """Embed a whole video on all ranks of `group`: every rank embeds its shard (+ halo) with
     `model.embed` and the embeddings / masks are all-gathered.  `patches`/`codec` hold the
@@ -49,25 +98,9 @@ def embed_sharded(model, patches, codec, refresh: int = 20, group=None, **embed_
     M = torch.as_tensor(M)
     if world == 1:
         return Z[:n_own], M[:n_own]
-    n_max = max(shard_frames(n_total, refresh, r, world)[1] for r in range(world))
-    zp = torch.zeros((n_max,) + tuple(Z.shape[1:]), dtype=Z.dtype, device=Z.device)
-    mp = torch.zeros((n_max,) + tuple(M.shape[1:]), dtype=M.dtype, device=M.device)
-    zp[:n_own] = Z[:n_own]
-    mp[:n_own] = M[:n_own]
-    zg = torch.empty((world * n_max,) + tuple(Z.shape[1:]), dtype=Z.dtype, device=Z.device)
-    mg = torch.empty((world * n_max,) + tuple(M.shape[1:]), dtype=M.dtype, device=M.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(zg, zp, group=group)
-        dist.all_gather_into_tensor(mg, mp, group=group)
-    else:                            # gloo (CPU tests): list form
-        dist.all_gather(list(zg.chunk(world)), zp, group=group)
-        dist.all_gather(list(mg.chunk(world)), mp, group=group)
-    parts_z, parts_m = [], []
-    for r in range(world):
-        _, n_r, _ = shard_frames(n_total, refresh, r, world)
-        parts_z.append(zg[r * n_max:r * n_max + n_r])
-        parts_m.append(mg[r * n_max:r * n_max + n_r])
-    return torch.cat(parts_z), torch.cat(parts_m)
+    counts = [shard_frames(n_total, refresh, r, world)[1] for r in range(world)]
+    Zg, Mg = gather_rows([Z, M], counts, group)
+    return Zg, Mg
 
 
 # ------------------------------------------------------------------ multi-video
@@ -147,26 +180,16 @@ def embed_videos_sharded(model, videos, costs=None, refresh: int = 20, group=Non
     outs = embed_videos(model, [videos[v] for v in mine], refresh, **embed_kw) if mine else []
     if world == 1:
         return [z for z, _ in outs]
-    D = None
-    for z, _ in outs:
-        D = z.shape[1]
-    if D is None:
-        D = int(model.cfg.dim)
-    dev = outs[0][0].device if outs else torch.device("cpu")
-    dt = outs[0][0].dtype if outs else torch.float32      # fp32 from libreusevit
-    n_rank = [sum(lens[v] for v in a) for a in assign]
-    n_max = max(n_rank)
-    zp = torch.zeros((n_max, D), dtype=dt, device=dev)
-    if outs:
-        zp[:n_rank[rank]] = torch.cat([z for z, _ in outs])
-    zg = torch.empty((world * n_max, D), dtype=dt, device=dev)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(zg, zp, group=group)
-    else:
-        dist.all_gather(list(zg.chunk(world)), zp, group=group)
+    D = int(outs[0][0].shape[1]) if outs else int(model.cfg.dim)
+    # a rank without videos contributes an empty block of the model's output dtype (fp32 for
+    # libreusevit); every rank must pass the same dtype to the collective
+    dt = outs[0][0].dtype if outs else getattr(model, "out_dtype", torch.float32)
+    z_mine = torch.cat([z for z, _ in outs]) if outs else torch.zeros((0, D), dtype=dt)
+    counts = [sum(lens[v] for v in a) for a in assign]
+    (zg,) = gather_rows([z_mine], counts, group)
     res = [None] * len(videos)
+    off = 0
     for r in range(world):
-        off = r * n_max
         for v in assign[r]:
             res[v] = zg[off:off + lens[v]]
             off += lens[v]

@@ -40,6 +40,8 @@ def test_shards_cover_and_plans_agree(n_total, world):
 
 class OracleModel:
     """Stand-in for ReuseViT.embed on a CPU rank: the fp64 oracle."""
+    out_dtype = torch.float64
+
     def __init__(self, cfg, W, G):
         self.cfg, self.W, self.G = cfg, W, G
 
@@ -179,5 +181,62 @@ def test_embed_videos_sharded_gloo_world2():
     G = synth.make_gates(cfg, restore_bias=True)
     for k, (n, p) in enumerate([(9, 0.1), (5, 0.4), (12, 0.2)]):
         x, c = synth.make_video(cfg, n, p, seed=2100 + k)
+        ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(n))
+        np.testing.assert_allclose(Zs[k], ref["Z"], rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ gather / max helpers (bench N > 1)
+def _worker_gather(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_14107_b200 import dist as rvdist
+    counts = [3, 0, 5][:world]                   # rank 1 owns nothing (fewer videos than ranks)
+    own = counts[rank]
+    Z = torch.full((own + 1, 4), float(rank)) + torch.arange(own + 1, dtype=torch.float32)[:, None]
+    M = torch.full((own + 1, 2, 3), rank, dtype=torch.uint8)
+    Zg, Mg = rvdist.gather_rows([Z, M], counts)
+    mx = rvdist.max_over_ranks(10.0 + rank)
+    # the videos path with more ranks than videos: a rank with no video still joins the gather
+    cfg = synth.CONFIGS["tiny"]
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=True)
+    import paper_2506_14107_b200.api as api
+    api.plan_gop = lambda n, refresh=20, reorder=True: oracle.plan_gop(n, refresh, reorder)
+    vids = []
+    for k, n in enumerate((6, 4)):
+        x, c = synth.make_video(cfg, n, 0.3, seed=2200 + k)
+        vids.append((torch.from_numpy(x), torch.from_numpy(c)))
+    Zs = rvdist.embed_videos_sharded(OracleModel(cfg, W, G), vids)
+    if rank == 0:
+        q.put((Zg.numpy(), Mg.numpy(), mx, [z.numpy() for z in Zs]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_rows_and_max_gloo_world3():
+    """The bench's N > 1 collective path on CPU: ragged per-rank blocks (one rank empty) gather
+    into rank order; the step time is the max over ranks; a rank without videos takes part."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_worker_gather, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    Zg, Mg, mx, Zs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    counts = [3, 0, 5]
+    wantZ = np.concatenate([np.full((n, 4), float(r)) + np.arange(n)[:, None] for r, n in enumerate(counts)])
+    wantM = np.concatenate([np.full((n, 2, 3), r, np.uint8) for r, n in enumerate(counts)])
+    assert np.array_equal(Zg, wantZ) and np.array_equal(Mg, wantM)
+    assert mx == 12.0
+    cfg = synth.CONFIGS["tiny"]
+    W = synth.make_vit(cfg, random_ln=True)
+    G = synth.make_gates(cfg, restore_bias=True)
+    for k, n in enumerate((6, 4)):
+        x, c = synth.make_video(cfg, n, 0.3, seed=2200 + k)
         ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(n))
         np.testing.assert_allclose(Zs[k], ref["Z"], rtol=0, atol=1e-12)

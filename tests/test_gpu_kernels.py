@@ -190,7 +190,12 @@ def test_attention_wave_kvsrc(dev, cfgname, use_tc):
 
 
 # ------------------------------------------------------------------------- score (teacher forced)
-@pytest.mark.parametrize("cfgname,mode,n", [("tiny", "continuous", 8), ("b16", "bimodal", 9), ("b16", "continuous", 9)])
+# generic (tiny), VPL = 6 (B/16, D = 768) and VPL = 8 (L/14 and L/14@336, D = 1024: the path the
+# bench runs) loops; bimodal (bench workloads) and continuous (s spread over (0, 1), tokens near
+# the threshold: SURVEY §8(d) continuous stress mode, tau = 0.3)
+@pytest.mark.parametrize("cfgname,mode,n", [("tiny", "continuous", 8), ("b16", "bimodal", 9), ("b16", "continuous", 9),
+                                            ("l14", "bimodal", 6), ("l14", "continuous", 6),
+                                            ("l14_336", "bimodal", 6), ("l14_336", "continuous", 6)])
 def test_score_teacher_forced(dev, cfgname, mode, n):
     cfg = synth.CONFIGS[cfgname]
     tau = 0.7 if mode == "bimodal" else 0.3
@@ -223,6 +228,18 @@ def test_score_teacher_forced(dev, cfgname, mode, n):
             band = np.abs(d_ref[f]) >= 1e-3
             assert np.array_equal(masks[f, l].cpu().numpy()[band], ref["M"][f, l][band])
             checked += band.sum()
+        # provider (Eq. 1 argmax, ties -> past) on frames with two references, wherever the two
+        # fp64 cosines differ by more than fp32 rounding can reorder
+        pv = wprov.cpu().numpy()
+        for k, f in enumerate(frames):
+            pa, fu = plan["past"][f], plan["future"][f]
+            if pa >= 0 and fu >= 0:
+                cur = X[f, 1:].astype(np.float64)
+                cos = lambda r: (cur * X[r, 1:]).sum(1) / np.sqrt((cur * cur).sum(1) * (X[r, 1:].astype(np.float64) ** 2).sum(1))
+                sp, sf = cos(pa), cos(fu)
+                clear = np.abs(sp - sf) > 1e-5
+                assert np.array_equal(pv[k, 1:][clear], (sf > sp)[clear].astype(np.uint8)), (l, f)
+                assert np.array_equal(ref["prov"][f, l][clear], (sf > sp)[clear].astype(np.int8))
         wm = wmask.cpu().numpy()
         assert np.all(wm[:, 0] == 0)
         assert np.array_equal(cntR.cpu().numpy(), wm.sum(1))
@@ -230,22 +247,25 @@ def test_score_teacher_forced(dev, cfgname, mode, n):
 
 
 # ------------------------------------------------------------------------- compaction
-@pytest.mark.parametrize("n_w,p", [(1, 0.5), (7, 0.0), (7, 1.0), (40, 0.3), (300, 0.9)])
-def test_compaction_bitexact(dev, n_w, p):
-    cfg = synth.CONFIGS["l14"]
-    m, _, _ = _model(synth.CONFIGS["tiny"], gates=False)
-    # compaction is independent of the model: T comes from the ctx config -> use a tiny ctx
-    cfg = synth.CONFIGS["tiny"]
-    T, N = cfg.T, cfg.N
-    rng = np.random.default_rng(n_w)
+def _compaction_case(dev, cfg, n_w, p, seed):
+    """Random level-wave of n_w frames (random slots, providers, masks at reuse rate p) through
+    rv_stage_compact; bit-exact vs oracle.compaction_indices (north star: compaction indices and
+    gathered token order bit-exact given the same mask)."""
+    from paper_2506_14107_b200 import ReuseViT
+    m = ReuseViT(cfg, 0)            # compaction needs only T from the context (no weights)
+    T = cfg.T
+    rng = np.random.default_rng(seed)
     masks = (rng.random((n_w, T)) < p).astype(np.uint8)
-    masks[:, 0] = 0
+    masks[:, 0] = rng.integers(0, 2, n_w)            # the kernel must ignore CLS's flag
     prov = (rng.random((n_w, T)) < 0.5).astype(np.uint8)
-    slots = rng.permutation(n_w + 5)[:n_w].astype(np.int32)
-    past = rng.integers(0, 50, n_w).astype(np.int32)
-    fut = rng.integers(0, 50, n_w).astype(np.int32)
+    n_slots = n_w + 7
+    slots = rng.permutation(n_slots)[:n_w].astype(np.int32)
+    past = rng.integers(0, n_slots, n_w).astype(np.int32)
+    fut = rng.integers(0, n_slots, n_w).astype(np.int32)
     wdesc = np.stack([slots, past, fut, np.ones(n_w, np.int32)], 1).astype(np.int32)
-    cntR = masks.sum(1).astype(np.int32)
+    cm = masks.copy()
+    cm[:, 0] = 0
+    cntR = cm.sum(1).astype(np.int32)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     idxC = torch.full((n_w * T,), -1, dtype=torch.int32, device=dev)
     idxR = torch.full((n_w * T,), -1, dtype=torch.int32, device=dev)
@@ -257,15 +277,33 @@ def test_compaction_bitexact(dev, n_w, p):
     torch.cuda.synchronize()
     eC, eR, eq = oracle.compaction_indices(masks)
     MC, MR = counts.cpu().tolist()
-    assert MC == len(eC) and MR == len(eR)
-    # map GPU global rows slot*T+tok back to wave-local rows w*T+tok
-    w_of_slot = {int(s): w for w, s in enumerate(slots)}
-    to_local = lambda r: np.array([w_of_slot[v // T] * T + v % T for v in r], np.int64)
-    assert np.array_equal(to_local(idxC[:MC].cpu().numpy()), eC)
-    assert np.array_equal(to_local(idxR[:MR].cpu().numpy()), eR)
+    assert MC == len(eC) and MR == len(eR) and MC + MR == n_w * T
+    # GPU rows are global slot*T + token; map back to the oracle's wave-local w*T + token
+    w_of_slot = np.full(n_slots, -1, np.int64)
+    w_of_slot[slots] = np.arange(n_w)
+    to_local = lambda r: w_of_slot[r // T] * T + r % T
+    gC = idxC[:MC].cpu().numpy().astype(np.int64)
+    gR = idxR[:MR].cpu().numpy().astype(np.int64)
+    assert np.array_equal(to_local(gC), eC)
+    assert np.array_equal(to_local(gR), eR)
     assert np.array_equal(qoff.cpu().numpy(), eq)
-    pr = provrow[:MR].cpu().numpy()
-    for r_loc, pg in zip(eR, pr):
-        w, tok = divmod(int(r_loc), T)
-        want = (fut[w] if prov[w, tok] else past[w]) * T + tok
-        assert pg == want
+    w, tok = eR // T, eR % T
+    want = np.where(prov[w, tok] == 1, fut[w], past[w]).astype(np.int64) * T + tok
+    assert np.array_equal(provrow[:MR].cpu().numpy().astype(np.int64), want)
+    # untouched tails
+    assert torch.all(idxC[MC:] == -1) and torch.all(idxR[MR:] == -1)
+    m.close()
+
+
+@pytest.mark.parametrize("n_w,p", [(1, 0.5), (7, 0.0), (7, 1.0), (40, 0.3), (300, 0.9)])
+def test_compaction_bitexact(dev, n_w, p):
+    _compaction_case(dev, synth.CONFIGS["tiny"], n_w, p, seed=n_w)
+
+
+# T = 257 (L/14) and 577 (L/14@336): several 256-token chunks per frame and a ragged tail;
+# n_w up to the 1,440 / 1,536-frame waves of the 7,200-frame bench (the O(n_w) offset sum)
+@pytest.mark.parametrize("cfgname", ["l14", "l14_336"])
+@pytest.mark.parametrize("n_w", [1, 45, 1440, 1536])
+@pytest.mark.parametrize("p", [0.0, 0.3, 0.9, 1.0])
+def test_compaction_bitexact_fullsize(dev, cfgname, n_w, p):
+    _compaction_case(dev, synth.CONFIGS[cfgname], n_w, p, seed=1000 * n_w + int(p * 10))

@@ -84,6 +84,41 @@ def test_embed_parity(cuda_ok, case):
     assert abs(st["reuse_all"] - Mg.sum() / (n * cfg.layers * cfg.T)) < 1e-9
 
 
+@pytest.mark.parametrize("cfgname,n,n_check", [("tiny", 12, 12), ("b16", 16, 16), ("l14", 9, 9)])
+def test_embed_parity_continuous(cuda_ok, cfgname, n, n_check):
+    """SURVEY §8(d) continuous stress mode, free running: x <- sqrt(1-a^2) x + a fresh spreads s
+    over (0, 1) and tau = 0.3 puts the gate threshold inside it, so (unlike the bimodal bench
+    workloads) many tokens sit near d = 0.  Asserts the north-star criteria on every frame:
+    masks agree on >= 99.9% of tokens with |d_oracle| >= 1e-3, embeddings within 2e-2 / cos
+    0.999 -- and compares the decision logits d themselves: the GPU's d (computed from its own
+    bf16-operand X) must follow the oracle's within the error the D10 tolerance on X allows.
+    A relative X error e shifts s by at most ~2e (1 - s <= 2 for any pair), so |dd| <=
+    |dd/ds| * 2e with |dd/ds| <= 16 * max QG' (~1.1) = 17.6; at the measured X error of
+    ~5e-3 (bf16 operands, fp32 residual) that is <= 0.18 * (1 + |d|)."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg, tau=0.3)
+    x, c = synth.make_video(cfg, n, 0.0, seed=2500 + n, mode="continuous")
+    plan = oracle.plan_gop(n)
+    Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), want_scores=True)
+    torch.cuda.synchronize()
+    frames = list(range(n_check))
+    ref = oracle.reuse_embed(cfg, W, G, x, c, plan, frames=frames)
+    err, cos = metrics(Z.cpu().numpy()[frames], ref["Z"][frames])
+    agree, cnt = mask_agreement(M.cpu().numpy(), ref, frames)
+    d_gpu = S.cpu().numpy()[frames].astype(np.float64)
+    d_ref = ref["d"][frames]
+    has = ~np.isnan(d_ref)
+    assert np.array_equal(np.isnan(d_gpu), ~has)
+    dd = np.abs(d_gpu[has] - d_ref[has]) / (1 + np.abs(d_ref[has]))
+    near = int((np.abs(d_ref[has]) < 1e-3).sum())
+    print(f"continuous {cfgname} n={n}: reuse_all={st['reuse_all']:.3f} max_err={err.max():.3e} "
+          f"min_cos={cos.min():.6f} mask_agree={agree:.5f} ({cnt} tokens, {near} in the band) "
+          f"|dd|/(1+|d|): median {np.median(dd):.2e} p99.9 {np.quantile(dd, 0.999):.2e} max {dd.max():.2e}")
+    assert err.max() <= 2e-2 and cos.min() >= 0.999 and agree >= 0.999
+    assert 0.05 < st["reuse_all"] < 0.95          # the threshold lies inside the s distribution
+    assert np.quantile(dd, 0.999) <= 0.18, np.quantile(dd, 0.999)
+
+
 @pytest.mark.parametrize("cfgname", ["tiny", "b16"])
 def test_dense_parity(cuda_ok, cfgname):
     """RV_DENSE (own-dense baseline): equals the plain ViT."""
@@ -253,44 +288,6 @@ def test_multi_video_embed_equals_per_video(cuda_ok, cfgname):
     ref = oracle.reuse_embed(cfg, W, G, x, c, oracle.plan_gop(5))
     err, cos = metrics(outs[1][0].cpu().numpy(), ref["Z"])
     assert err.max() <= 2e-2 and cos.min() >= 0.999
-
-
-_FUSED_SCRIPT = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, sys.argv[1])
-import synth
-from paper_2506_14107_b200 import ReuseViT
-cfg = synth.CONFIGS[sys.argv[2]]
-W, G = synth.make_vit(cfg), synth.make_gates(cfg)
-m = ReuseViT(cfg, 0)
-m.load_vit(synth.pack_vit(cfg, W))
-m.load_gates(synth.pack_gates(cfg, G))
-x, c = synth.make_video(cfg, 41, 0.3, seed=21)
-Z, M, _, _ = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda())
-torch.cuda.synchronize()
-np.save(sys.argv[3], np.concatenate([Z.cpu().numpy().view(np.uint32).ravel().astype(np.int64),
-                                     M.cpu().numpy().ravel().astype(np.int64)]))
-"""
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("cfgname", ["b16", "l14"])
-def test_fused_score_r1_bitwise_equal(cuda_ok, cfgname, tmp_path):
-    """The opt-in fused decision + R1 kernel (RV_SCORE_R1=1, k_score_r1.cu) computes the same
-    fp32 decision arithmetic and the same bf16 Delta / K order as score_kernel + the R1 GEMM:
-    embeddings and masks are bitwise equal to the default path (run in subprocesses because the
-    switch is read once per process)."""
-    import subprocess
-    import sys
-    outs = []
-    for flag in ("0", "1"):
-        f = tmp_path / f"out{flag}.npy"
-        env = dict(os.environ, RV_SCORE_R1=flag)
-        r = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, ROOT, cfgname, str(f)], env=env,
-                           capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(np.load(f))
-    assert np.array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("cfgname,n", [("l14", 1), ("l14", 2), ("b16", 3), ("b16", 21), ("b16", 22), ("l14", 40)])

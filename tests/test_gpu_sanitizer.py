@@ -1,0 +1,79 @@
+"""compute-sanitizer memcheck / racecheck / synccheck (SURVEY §4 and §5 "race detection") over
+the tiny config's whole embed (every kernel of the path: score, compaction, gathers, tcgen05
+GEMMs, attention, restoration, ln_post; graph off so every launch is checked individually)
+and one L/14 level-wave of the tcgen05 attention kernel (d_h = 64, T = 257, reuse-cache
+indirection).  Each tool must report zero errors."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_2506_14107_b200 import ReuseViT
+cfg = synth.CONFIGS["tiny"]
+m = ReuseViT(cfg, 0)
+m.load_vit(synth.pack_vit(cfg, synth.make_vit(cfg, random_ln=True)))
+m.load_gates(synth.pack_gates(cfg, synth.make_gates(cfg, restore_bias=True)))
+x, c = synth.make_video(cfg, 8, 0.3, seed=2000)
+Z, M, S, st = m.embed(torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda(), want_scores=True, graph=False)
+torch.cuda.synchronize()
+assert np.isfinite(Z.cpu().numpy()).all()
+m.close()
+# one L/14 wave of the tcgen05 attention (stage entry point, rv_stage_attention)
+cfg = synth.CONFIGS[sys.argv[2]]
+m = ReuseViT(cfg, 0)
+m.load_vit(synth.pack_vit(cfg, synth.make_vit(cfg)))
+T, D, H = cfg.T, cfg.dim, cfg.heads
+n_w = 12
+rng = np.random.default_rng(5)
+nq = rng.integers(20, 80, n_w); nq[0] = T; nq[1] = 1
+qoff = np.concatenate([[0], np.cumsum(nq)]).astype(np.int32)
+kvsrc = np.arange(n_w * T, dtype=np.int32).reshape(n_w, T)
+reuse = rng.random((n_w, T)) < 0.7; reuse[:, 0] = False
+kvsrc[reuse] = (rng.integers(0, n_w, (n_w, T)) * T + np.arange(T)[None, :])[reuse]
+wdesc = np.zeros((n_w, 4), np.int32); wdesc[:, 0] = np.arange(n_w)
+dev = torch.device("cuda:0")
+q = torch.randn(int(qoff[-1]), D, device=dev).to(torch.bfloat16)
+KV = torch.randn(n_w * T, 2 * D, device=dev).to(torch.bfloat16)
+out = torch.zeros((int(qoff[-1]), D), dtype=torch.bfloat16, device=dev)
+pcls = torch.zeros((n_w, H, cfg.N), dtype=torch.float32, device=dev)
+m.stage_attention(torch.from_numpy(wdesc).to(dev), torch.from_numpy(qoff).to(dev), q, KV, out, pcls,
+                  torch.cuda.current_stream(), use_tc=True, kvsrc=torch.from_numpy(kvsrc).to(dev))
+torch.cuda.synchronize()
+assert torch.isfinite(out.float()).all()
+print("SANITIZER_SCRIPT_OK")
+"""
+
+
+def _sanitizer():
+    for p in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if p and os.path.exists(p):
+            return p
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(cuda_ok, tool, tmp_path):
+    script = tmp_path / "san.py"
+    script.write_text(_SCRIPT)
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "9", "--target-processes", "all"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, str(script), ROOT, "l14"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
+    log = r.stdout[-6000:] + r.stderr[-6000:]
+    print(log[-3000:])
+    assert "SANITIZER_SCRIPT_OK" in r.stdout, log
+    assert r.returncode == 0, log
+    import re
+    summ = re.findall(r"(ERROR|RACECHECK) SUMMARY: .*", log)
+    assert summ, log
+    assert all(re.search(r"\b0 (errors|hazards)", x) for x in summ), summ

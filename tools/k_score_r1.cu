@@ -1,3 +1,6 @@
+// ARCHIVED EXPERIMENT (not compiled into libreusevit; kept for the record of round 1):
+// fused decision + R1 on the tensor cores.  Bitwise equal to score_kernel + the R1 GEMM but
+// 201 ms per step vs 83 + 17 unfused.  Built only by hand against csrc/.
 // k_score_r1.cu — reuse decision fused with the first restoration layer (SURVEY §8(a) a2+a3 and
 // the R1 half of a12; Eq. 1-4, Eq. 8-9).
 //
