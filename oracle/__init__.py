@@ -23,3 +23,7 @@ from .reusevit_ref import (  # noqa: F401
 )
 from .store_ref import to_fp16, cosine_scores, topk_cosine, storage_bytes_per_second  # noqa: F401
 from .chain_ref import reuse_embed_chain  # noqa: F401
+from .train_ref import (  # noqa: F401
+    GROUP_PATTERN, group_plan, gumbel_soft_mask, soft_forward, group_losses, gates_to_torch, batch_loss,
+    loss_and_grads, adam_step, temperature,
+)

@@ -27,7 +27,8 @@ import numpy as np
 
 __all__ = [
     "ViTConfig", "CONFIGS", "make_vit", "make_gates", "make_video", "make_video_torch",
-    "pack_vit", "pack_gates", "vit_array_order", "gate_array_order",
+    "pack_vit", "pack_gates", "vit_array_order", "gate_array_order", "make_gumbel", "make_train_groups",
+    "init_train_gates",
 ]
 
 
@@ -240,3 +241,38 @@ def make_video_torch(cfg: ViTConfig, n: int, p: float, seed: int = 2000, device=
     if n > 1:
         codec[1:] = ((x[1:] - x[:-1]) ** 2).mean(dim=2).sqrt()
     return x, codec
+
+
+def make_gumbel(shape, seed: int) -> np.ndarray:
+    """Standard Gumbel(0, 1) draws -log(-log(U)), U ~ U(0, 1) (PCG64), float32: the random
+    numbers Eq. 11's Gumbel-Softmax draws, passed to both sides as inputs."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    u = rng.random(shape)
+    u = np.clip(u, 1e-12, 1.0 - 1e-12)
+    return (-np.log(-np.log(u))).astype(np.float32)
+
+
+def make_train_groups(cfg: ViTConfig, B: int, display, seed: int, p_range=(0.05, 0.4)):
+    """B training groups (P:478-482 grouped frames): each group is drawn from its own
+    ``max(display)+1``-frame bimodal clip with motion p ~ U(p_range); returns the frames at the
+    given 0-based display indices (ascending) as (patches [B, G, N, pp], codec [B, G, N]).
+    The codec stub stays relative to the previous DISPLAY frame of the clip."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    disp = sorted(int(d) for d in display)
+    n = disp[-1] + 1
+    xs, cs = [], []
+    for b in range(B):
+        p = float(rng.uniform(*p_range))
+        x, c = make_video(cfg, n, p, seed=int(rng.integers(1 << 31)))
+        xs.append(x[disp])
+        cs.append(c[disp])
+    return np.stack(xs), np.stack(cs)
+
+
+def init_train_gates(cfg: ViTConfig, seed: int = 1236) -> Dict[str, np.ndarray]:
+    """Initial gates of a training run ("restoration MLP's final layer is
+    zero-initialized; decision MLP final bias initialized to -1 (recompute-leaning)"):
+    decision and first restoration layer ~ N(0, 0.02), Wr2 = 0, biases 0, bd2 = -1."""
+    return make_gates(cfg, seed=seed, structured=False, final_bias=-1.0, restore_bias=False,
+                      restore_std=0.02) | {f"L{l}.Wr2": np.zeros((cfg.hidden_r, cfg.dim), np.float32)
+                                          for l in range(cfg.layers)}
