@@ -45,6 +45,21 @@ class RvKernelProf(ctypes.Structure):
                 ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
+class RvTrainConfig(ctypes.Structure):
+    _fields_ = [("groups", c_i32), ("group_size", c_i32), ("type", ctypes.POINTER(ctypes.c_int8)),
+                ("past", ctypes.POINTER(c_i32)), ("future", ctypes.POINTER(c_i32)), ("order", ctypes.POINTER(c_i32)),
+                ("alpha", ctypes.c_float), ("r_target", ctypes.c_float), ("lr", ctypes.c_float),
+                ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float)]
+
+
+class RvTrainLog(ctypes.Structure):
+    _fields_ = [("l_sim", ctypes.c_double), ("l_reuse", ctypes.c_double), ("l_total", ctypes.c_double),
+                ("cos_mean", ctypes.c_double), ("step", c_i32)]
+
+
+RV_TRAIN_DENSE, RV_TRAIN_FORCE = 1, 2
+
+
 class ReuseViTError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
@@ -75,6 +90,17 @@ SIGNATURES = {
     "rv_wave_counts": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
     "rv_f32_to_f16": (c_i32, [c_vp, c_vp, ctypes.c_int64, c_vp]),
     "rv_topk_cosine": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    # gate trainer (include/reusevit_train.h)
+    "rv_trainer_create": (c_i32, [ctypes.POINTER(RvConfig), ctypes.c_int, P_f32, c_sz, P_f32, c_sz,
+                                  ctypes.POINTER(RvTrainConfig), ctypes.POINTER(c_vp)]),
+    "rv_trainer_forward": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, ctypes.c_float, c_u32, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp]),
+    "rv_trainer_loss_grad": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, ctypes.c_float, c_vp, ctypes.POINTER(RvTrainLog),
+                                     c_vp]),
+    "rv_trainer_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, ctypes.c_float, ctypes.POINTER(RvTrainLog), c_vp]),
+    "rv_trainer_gates": (c_i32, [c_vp, P_f32]),
+    "rv_trainer_last_error": (ctypes.c_char_p, [c_vp]),
+    "rv_trainer_destroy": (None, [c_vp]),
 }
 
 _LIB = None
