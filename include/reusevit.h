@@ -100,9 +100,11 @@ typedef struct {
                               compaction (results identical, only the batching differs)         */
 #define RV_CHAIN 128u      /* SPEC chain variant: the
                               decision on the FFN input x'_l gates FFN_l -> QKV_{l+1}; attention
-                              and W_o dense for all tokens (mma.sync attention path)            */
-#define RV_ATTN_SYNC 32u   /* attention on the mma.sync kernel (k_attn.cu) even where the default
-                              tcgen05/TMEM kernel (k_attn_tc.cu: d_h = 64, T - 1 <= 256) applies */
+                              and W_o dense for all tokens (general tcgen05 attention, q read
+                              from the q|k|v cache through the source-row table)                */
+#define RV_ATTN_SYNC 32u   /* diagnostic: attention on the mma.sync kernel (k_attn.cu) even where the
+                              tcgen05/TMEM kernels (k_attn_tc.cu: d_h = 64) apply; without it the
+                              mma.sync kernel runs only for d_h = 16 (the tiny config)            */
 
 /* Per-kernel-class profile of the last RV_PROFILE embed (rv_profile). */
 typedef struct {

@@ -69,8 +69,10 @@ rv_status rv_stage_gemm_rows(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const
  * layer.  q_rows = allocated rows of q (>= qoff[n_w]; the tcgen05 path
  * reads q with TMA in 64-row tiles).  kvsrc [slots][T] int32 (or NULL = identity) is the
  * reuse-cache row table of a7: key j of the frame in slot s is row kvsrc[s*T + j] of KV.
- * use_tc selects the tcgen05/TMEM kernel (d_h = 64, T - 1 <= 256; RV_ECONTRACT otherwise),
- * else the mma.sync kernel (any supported shape). */
+ * use_tc: 0 the mma.sync kernel (any supported shape); 1 the tcgen05/TMEM kernels (the
+ * persistent one for T - 1 <= 256, else the general one); 2 the general tcgen05 kernel
+ * (128-query tiles, online softmax over 128-key blocks, d_h = 64, T <= 1024).  RV_ECONTRACT
+ * when the shape is outside the selected kernel's range. */
 rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc,
                              const int32_t* qoff, const void* q, int32_t q_rows, const void* KV,
                              const int32_t* kvsrc, void* out, float* pcls, int32_t use_tc,

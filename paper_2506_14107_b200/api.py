@@ -242,7 +242,8 @@ class ReuseViT:
         return out
 
     def stage_attention(self, wdesc, qoff, q, KV, out, pcls, stream, use_tc=False, kvsrc=None):
+        """use_tc: False/0 mma.sync, True/1 tcgen05 (persistent kernel where T <= 257), 2 general tcgen05."""
         check(self.lib, self.lib.rv_stage_attention(self.h, wdesc.shape[0], _ptr(wdesc), _ptr(qoff), _ptr(q),
                                                     q.shape[0], _ptr(KV), _ptr(kvsrc), _ptr(out), _ptr(pcls),
-                                                    1 if use_tc else 0,
+                                                    int(use_tc),
                                                     ctypes.c_void_p(stream.cuda_stream)), self.h)

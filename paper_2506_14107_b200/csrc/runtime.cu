@@ -474,10 +474,14 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       r.begin(K_ATTN,l,wi);
       {
         float* pcl = (!dense && l + 1 < L) ? ctx->pclsh : nullptr;
-        if (!(flags & RV_ATTN_SYNC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM kernel (default)
+        if (!(flags & RV_ATTN_SYNC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM, T <= 257 (default)
           r.chk(launch_attention_tc(ctx->tmQ, ctx->tmKV, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
-        else
+        else if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05/TMEM, any T (L/14@336)
+          r.chk(launch_attention_tcg(ctx->q, D, 0, 0, ctx->KV, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T,
+                                     D, H, s),
+                "attention");
+        else   // mma.sync kernel: d_h = 16 (tiny config) or RV_ATTN_SYNC
           r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
       }
@@ -619,9 +623,14 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       const int maxC = rows;
       // dense attention of every token over all keys of its frame
       r.begin(K_ATTN,l,wi);
-      r.chk(launch_attention(nullptr, Qc, KS[l & 1], ctx->att, wd, ctx->qoffT, (!dense && l + 1 < L) ? P[l & 1] : nullptr,
-                             n_w, T, D, H, s, ld3, 1),
-            "attention");
+      float* pcl_chain = (!dense && l + 1 < L) ? P[l & 1] : nullptr;
+      if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05: q from the cache via the table
+        r.chk(launch_attention_tcg(Qc, ld3, 2 * D, 1, Qc, ld3, KS[l & 1], ctx->att, wd, ctx->qoffT, pcl_chain, n_w, T, D,
+                                   H, s),
+              "attention");
+      else
+        r.chk(launch_attention(nullptr, Qc, KS[l & 1], ctx->att, wd, ctx->qoffT, pcl_chain, n_w, T, D, H, s, ld3, 1),
+              "attention");
       // W_o + residual for every token: x'_l (the chain input) into the XP cache
       {
         Epi e;
@@ -1310,8 +1319,13 @@ rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, con
   if (!ctx) return RV_ECONTRACT;
   if (q_rows < 1 || !q || !KV || !out) return fail(ctx, RV_ECONTRACT, "rv_stage_attention: bad arguments");
   CK(cudaSetDevice(ctx->device));
-  if (use_tc && !attn_tc_supported(ctx->T, ctx->D, ctx->H))
-    return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and T - 1 <= 256");
+  if (use_tc == 2 || (use_tc == 1 && !attn_tc_supported(ctx->T, ctx->D, ctx->H))) {   // general tcgen05 kernel
+    if (!attn_tcg_supported(ctx->T, ctx->D, ctx->H))
+      return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and T <= 1024");
+    CK(launch_attention_tcg((const bf16*)q, ctx->D, 0, 0, (const bf16*)KV, 2LL * ctx->D, kvsrc, (bf16*)out, wdesc, qoff,
+                            pcls, n_w, ctx->T, ctx->D, ctx->H, (cudaStream_t)stream));
+    return RV_OK;
+  }
   if (use_tc) {
     // K/V rows the wave can address: slots 0..max(slot); the tensor map needs the extent
     std::vector<int32_t> wd((size_t)n_w * 4);

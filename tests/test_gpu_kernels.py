@@ -104,8 +104,11 @@ def test_gemm_row_mapped_epilogue_vs_torch(dev, M, N, K, act):
 
 
 # ------------------------------------------------------------------------- attention
+# use_tc: False mma.sync; True tcgen05 (persistent kernel for T <= 257, general kernel for
+# T = 577); 2 the general tcgen05 kernel (128-query tiles, online softmax over key blocks)
 @pytest.mark.parametrize("cfgname,use_tc", [("tiny", False), ("b16", False), ("l14", False), ("l14_336", False),
-                                            ("b16", True), ("l14", True)])
+                                            ("b16", True), ("l14", True), ("l14_336", True), ("b16", 2),
+                                            ("l14", 2)])
 def test_attention_vs_torch(dev, cfgname, use_tc):
     cfg = synth.CONFIGS[cfgname]
     m, _, _ = _model(cfg, gates=False)
@@ -140,7 +143,7 @@ def test_attention_vs_torch(dev, cfgname, use_tc):
 
 
 @pytest.mark.parametrize("cfgname,use_tc", [("b16", False), ("l14", False), ("l14_336", False), ("b16", True),
-                                            ("l14", True)])
+                                            ("l14", True), ("l14_336", True), ("l14", 2)])
 def test_attention_wave_kvsrc(dev, cfgname, use_tc):
     """A level-wave-sized launch: 300 frames in shuffled slots, ragged query counts (1 .. T,
     mostly the 30-70 of the paper's reuse rates), K/V rows read through a random reuse-cache
@@ -187,6 +190,43 @@ def test_attention_wave_kvsrc(dev, cfgname, use_tc):
         worst_p = max(worst_p, (pcls[s] - P[:, 0, 1:]).abs().max().item())
     assert worst < 2e-2, worst
     assert worst_p < 1e-4, worst_p
+
+
+@pytest.mark.parametrize("boost_block", [0, 2, 4])
+def test_attention_tcg_online_rescale(dev, boost_block):
+    """The general tcgen05 kernel's lazy online softmax: keys of one 128-key block are scaled
+    up 6x so that block dominates the row maxima.  Block 0 boosted: no later rescale; blocks
+    2 / 4 (the ragged last block of T = 577): the running max jumps by far more than 2^8 and
+    O in TMEM is rescaled mid-row.  Output and CLS probabilities vs torch fp32."""
+    cfg = synth.CONFIGS["l14_336"]
+    m, _, _ = _model(cfg, gates=False)
+    T, D, H, dh = cfg.T, cfg.dim, cfg.heads, cfg.dh
+    g = torch.Generator(device=dev).manual_seed(40 + boost_block)
+    n_w = 3
+    nq = np.array([T, 130, 1])
+    qoff = np.concatenate([[0], np.cumsum(nq)]).astype(np.int32)
+    q = torch.randn(int(qoff[-1]), D, device=dev, generator=g).to(torch.bfloat16)
+    KVf = torch.randn(n_w * T, 2 * D, device=dev, generator=g)
+    for w in range(n_w):
+        lo = w * T + boost_block * 128
+        KVf[lo:min(lo + 128, (w + 1) * T), :D] *= 6.0
+    KV = KVf.to(torch.bfloat16)
+    wdesc = np.zeros((n_w, 4), np.int32)
+    wdesc[:, 0] = np.arange(n_w)
+    out = torch.zeros((int(qoff[-1]), D), dtype=torch.bfloat16, device=dev)
+    pcls = torch.zeros((n_w, H, cfg.N), dtype=torch.float32, device=dev)
+    m.stage_attention(torch.from_numpy(wdesc).to(dev), torch.from_numpy(qoff).to(dev), q, KV, out, pcls,
+                      torch.cuda.current_stream(), use_tc=2)
+    torch.cuda.synchronize()
+    for w in range(n_w):
+        Kf = KV[w * T:(w + 1) * T, :D].float().reshape(T, H, dh).transpose(0, 1)
+        Vf = KV[w * T:(w + 1) * T, D:].float().reshape(T, H, dh).transpose(0, 1)
+        qf = q[qoff[w]:qoff[w + 1]].float().reshape(-1, H, dh).transpose(0, 1)
+        P = torch.softmax(qf @ Kf.transpose(1, 2) / dh ** 0.5, dim=-1)
+        ref = (P @ Vf).transpose(0, 1).reshape(-1, D)
+        got = out[qoff[w]:qoff[w + 1]].float()
+        assert (got - ref).abs().max().item() < 2e-2 * (1 + ref.abs().max().item())
+        assert (pcls[w] - P[:, 0, 1:]).abs().max().item() < 1e-4
 
 
 # ------------------------------------------------------------------------- score (teacher forced)
