@@ -80,13 +80,15 @@ typedef struct {
   double flops_exec;          /* executed tensor FLOPs (SURVEY §8(d) F_exec formula)            */
   double flops_dense;         /* same frames with no reuse                                      */
   double bytes_alg;           /* algorithmic HBM bytes of the reuse path (DESIGN.md §6 model)  */
-  uint64_t peak_cache_bytes;  /* device bytes of the layer-wise cache (X ping-pong + K/V)       */
+  uint64_t peak_cache_bytes;  /* allocated bytes of the activation cache: X ping-pong + one K/V
+                                 layer, or every layer's X and K/V with RV_KEEP_ALL_CACHE         */
   uint64_t keepall_cache_bytes; /* bytes if every layer's X and K/V were kept (Fig. 12 analog) */
   float ms_total;             /* device time of the embed (CUDA events, H2D/D2H included)      */
   float ms_compute;           /* device time of the compute graph only                          */
   int32_t n_levels;           /* dependency levels (waves per layer)                            */
   int32_t n_launches;         /* kernels launched by the last embed (own kernels only)          */
   float reuse_by_layer[64];   /* per-layer Eq. 14 reuse rate over non-I frames                  */
+  uint64_t device_bytes;      /* bytes of every per-embed device buffer the context allocated   */
 } rv_stats;
 
 /* rv_embed flags */
@@ -102,6 +104,13 @@ typedef struct {
                               decision on the FFN input x'_l gates FFN_l -> QKV_{l+1}; attention
                               and W_o dense for all tokens (general tcgen05 attention, q read
                               from the q|k|v cache through the source-row table)                */
+#define RV_NO_COMPACTION 256u  /* ablation (SURVEY §8(d) ladder step 1, "masked dense"): every token
+                              is recomputed (no stream compaction), then the reused tokens'
+                              outputs are overwritten by the restoration; results equal the
+                              compacted path bitwise (row-local kernels)                         */
+#define RV_KEEP_ALL_CACHE 512u /* ablation of cached memory compaction (Fig. 12
+                              analogue): keep every layer's X and K/V allocated; at the 7,200-frame
+                              workload this needs ~371 GB and fails with RV_ENOMEM               */
 #define RV_ATTN_SYNC 32u   /* diagnostic: attention on the mma.sync kernel (k_attn.cu) even where the
                               tcgen05/TMEM kernels (k_attn_tc.cu: d_h = 64) apply; without it the
                               mma.sync kernel runs only for d_h = 16 (the tiny config)            */

@@ -178,36 +178,42 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
 
 constexpr int COMPACT_THREADS = 256;
 
+// all_c (RV_NO_COMPACTION, the ablation's "masked dense" step): every token of every frame is in
+// the recompute list (idxC = all rows in order, qoff[w] = w*T) while idxR / provrow still list
+// the reused tokens, whose outputs the restoration then overwrites.  Outputs are bitwise those
+// of the compacted path (row-local GEMMs and attention rows are batch-invariant).
 __global__ void __launch_bounds__(COMPACT_THREADS)
     compact_kernel(int n_w, int T, const int4* __restrict__ wdesc, const uint8_t* __restrict__ wmask,
                    const uint8_t* __restrict__ wprov, const int* __restrict__ cntR, int* __restrict__ idxC,
                    int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
                    int* __restrict__ counts, int* kvsrc, unsigned long long* reuse_ctr, int* count_log,
-                   int* __restrict__ rpos) {
+                   int* __restrict__ rpos, int all_c) {
   __shared__ int s_part[COMPACT_THREADS / 32];
   __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
   __shared__ int s_base[2];
   const int w = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // offC = sum_{v<w} |C_v| (exact integer reduction)
+  // offR = sum_{v<w} |R_v| (exact integer reduction); offC = w*T - offR (or w*T: all_c)
   int part = 0;
-  for (int v = threadIdx.x; v < w; v += COMPACT_THREADS) part += T - cntR[v];
+  for (int v = threadIdx.x; v < w; v += COMPACT_THREADS) part += cntR[v];
   part = warp_sum_i(part);
   if (lane == 0) s_part[warp] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int off = 0;
-    for (int k = 0; k < COMPACT_THREADS / 32; ++k) off += s_part[k];
-    s_base[0] = off;                 // C offset
-    s_base[1] = w * T - off;         // R offset (|R_v| = T - |C_v|)
-    qoff[w] = off;
+    int offR = 0;
+    for (int k = 0; k < COMPACT_THREADS / 32; ++k) offR += s_part[k];
+    const int offC = all_c ? w * T : w * T - offR;
+    s_base[0] = offC;
+    s_base[1] = offR;
+    qoff[w] = offC;
     if (w == n_w - 1) {
-      const int tot = off + T - cntR[w];
-      qoff[n_w] = tot;
-      counts[0] = tot;
-      counts[1] = n_w * T - tot;
-      if (reuse_ctr) atomicAdd(reuse_ctr, (unsigned long long)(n_w * T - tot));
-      if (count_log) { count_log[0] = tot; count_log[1] = n_w * T - tot; }
+      const int totR = offR + cntR[w];
+      const int totC = all_c ? n_w * T : n_w * T - totR;
+      qoff[n_w] = totC;
+      counts[0] = totC;
+      counts[1] = totR;
+      if (reuse_ctr) atomicAdd(reuse_ctr, (unsigned long long)totR);
+      if (count_log) { count_log[0] = totC; count_log[1] = totR; }
     }
   }
   __syncthreads();
@@ -219,8 +225,8 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
   for (int base = 0; base < T; base += COMPACT_THREADS) {
     const int i = base + threadIdx.x;
     const bool valid = i < T;
-    const bool isC = valid && (i == 0 || mk[i] == 0);
-    const bool isR = valid && !isC;
+    const bool isR = valid && i > 0 && mk[i] != 0;
+    const bool isC = valid && (all_c || !isR);
     const unsigned bc = __ballot_sync(0xffffffffu, isC);
     const unsigned br = __ballot_sync(0xffffffffu, isR);
     if (lane == 0) { s_wc[warp] = __popc(bc); s_wr[warp] = __popc(br); }
@@ -233,9 +239,11 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
     }
     const unsigned lt = (1u << lane) - 1u;
     if (isC) {
-      if (rpos) rpos[(long long)w * T + i] = -1;   // restoration row map: not reused
       idxC[offC + pc + __popc(bc & lt)] = slot * T + i;
-      if (kvsrc) kvsrc[(long long)slot * T + i] = slot * T + i;
+      if (!isR) {
+        if (rpos) rpos[(long long)w * T + i] = -1;   // restoration row map: not reused
+        if (kvsrc) kvsrc[(long long)slot * T + i] = slot * T + i;
+      }
     }
     if (isR) {
       const int r = offR + pr + __popc(br & lt);
@@ -276,11 +284,11 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
 
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s) {
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s, int all_c) {
   if (n_w <= 0) return cudaSuccess;
   compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
                                                  cntR, idxC, idxR, provrow, qoff, counts, kvsrc, reuse_ctr, count_log,
-                                                 rpos);
+                                                 rpos, all_c);
   return cudaGetLastError();
 }
 

@@ -68,6 +68,13 @@ struct rv_ctx {
   std::vector<void*> ballocs;
   float* X[2] = {nullptr, nullptr};
   bf16* KV = nullptr;
+  // RV_KEEP_ALL_CACHE (cached memory compaction disabled, P:502-522 ablation): every layer's X
+  // [L+1][n][T][D] and K/V [L][n][T][2D] stay allocated instead of the ping-pong / single layer
+  bool keepall = false;
+  float* Xall = nullptr;
+  bf16* KVall = nullptr;
+  std::vector<CUtensorMap> tmKVl;
+  unsigned long long cache_bytes = 0, alloc_bytes = 0;   // allocated bytes: X + K/V cache, all per-embed buffers
   float* pclsh = nullptr;     // [n][H][N] per-head CLS attention of the previous layer (t)
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
   bf16* dfull = nullptr;      // [max_w][T][D] Delta of reused tokens (wave-local token rows, bf16)
@@ -271,6 +278,8 @@ void release_buffers(rv_ctx* ctx) {
   free_list(ctx->ballocs);
   ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0; ctx->chain_cap = 0;
   ctx->X[0] = ctx->X[1] = nullptr; ctx->KV = nullptr; ctx->pclsh = nullptr; ctx->kvsrc = nullptr;
+  ctx->Xall = nullptr; ctx->KVall = nullptr; ctx->keepall = false; ctx->tmKVl.clear();
+  ctx->cache_bytes = ctx->alloc_bytes = 0;
   ctx->dfull = nullptr; ctx->rpos = nullptr; ctx->patches_bf16 = nullptr; ctx->wdesc = nullptr;
   ctx->wmask = ctx->wprov = nullptr;
   ctx->cntR = ctx->idxC = ctx->idxR = ctx->provrow = ctx->qoff = ctx->counts = nullptr;
@@ -279,10 +288,12 @@ void release_buffers(rv_ctx* ctx) {
   ctx->wrows = nullptr; ctx->qoffT = nullptr;
 }
 
-rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int max_w) {
+rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int max_w, bool keepall) {
   capC = (capC + 127) / 128 * 128;
   capR = std::max<long long>(128, (capR + 127) / 128 * 128);
-  if (n <= ctx->n_cap && capC <= ctx->capC && capR <= ctx->capR && max_w <= ctx->wdesc_cap) return RV_OK;
+  if (n <= ctx->n_cap && capC <= ctx->capC && capR <= ctx->capR && max_w <= ctx->wdesc_cap && keepall == ctx->keepall)
+    return RV_OK;
+  if (keepall != ctx->keepall) release_buffers(ctx);   // switching modes: start from the request's sizes
   n = std::max(n, ctx->n_cap);
   capC = std::max(capC, ctx->capC);
   capR = std::max(capR, ctx->capR);
@@ -291,10 +302,22 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   const long long T = ctx->T, D = ctx->D, N = ctx->N;
   auto& B = ctx->ballocs;
   rv_status s;
-#define AL(ptr, cnt) if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) { release_buffers(ctx); return s; }
-  AL(ctx->X[0], n * T * D);
-  AL(ctx->X[1], n * T * D);
-  AL(ctx->KV, n * T * 2 * D);
+  const long long L = ctx->L;
+  unsigned long long bytes = 0;
+#define AL(ptr, cnt)                                                                 \
+  if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) { release_buffers(ctx); return s; } \
+  bytes += (unsigned long long)(cnt) * sizeof(*ptr)
+  if (keepall) {
+    AL(ctx->Xall, (L + 1) * n * T * D);
+    AL(ctx->KVall, L * n * T * 2 * D);
+    ctx->X[0] = ctx->Xall;
+    ctx->KV = ctx->KVall;
+  } else {
+    AL(ctx->X[0], n * T * D);
+    AL(ctx->X[1], n * T * D);
+    AL(ctx->KV, n * T * 2 * D);
+  }
+  const unsigned long long cache = bytes;
   AL(ctx->pclsh, n * ctx->H * N);
   AL(ctx->kvsrc, n * T);
   AL(ctx->dfull, (size_t)max_w * T * D);
@@ -326,7 +349,12 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   bool ok = make_tmap_bf16(&ctx->tmQ, ctx->q, capC, (int)D, 64, e, sizeof e) &&
             make_tmap_bf16(&ctx->tmKV, ctx->KV, (long long)n * T, 2 * (int)D, 1, e, sizeof e) &&
             gemm_make_plan(&ctx->pe, ctx->patches_bf16, (long long)n * N, ctx->W_pe, (int)D, ctx->KP, e, sizeof e);
-  const int L = ctx->L;
+  if (ok && keepall) {
+    ctx->tmKVl.resize(L);
+    for (int l = 0; ok && l < L; ++l)
+      ok = make_tmap_bf16(&ctx->tmKVl[l], ctx->KVall + (size_t)l * n * T * 2 * D, (long long)n * T, 2 * (int)D, 1, e,
+                          sizeof e);
+  }
   ctx->g_qkv.resize(L); ctx->g_wo.resize(L); ctx->g_fc1.resize(L); ctx->g_fc2.resize(L);
   ctx->g_r1.resize(L); ctx->g_r2.resize(L);
   for (int l = 0; ok && l < L; ++l) {
@@ -347,6 +375,9 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   ctx->capC = capC;
   ctx->capR = capR;
   ctx->wdesc_cap = max_w;
+  ctx->keepall = keepall;
+  ctx->cache_bytes = cache;
+  ctx->alloc_bytes = bytes;
   return RV_OK;
 }
 
@@ -430,10 +461,14 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   r.begin(K_EMBED,-1,-1);
   r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
         "embed_finish");
+  const bool keepall = ctx->keepall;
+  const size_t nTD = (size_t)ctx->n_cap * T * D;
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
-    float* Xin = ctx->X[l & 1];
-    float* Xout = ctx->X[(l + 1) & 1];
+    float* Xin = keepall ? ctx->Xall + (size_t)l * nTD : ctx->X[l & 1];
+    float* Xout = keepall ? ctx->Xall + (size_t)(l + 1) * nTD : ctx->X[(l + 1) & 1];
+    bf16* KVl = keepall ? ctx->KVall + (size_t)l * 2 * nTD : ctx->KV;
+    const CUtensorMap& tmKVl = keepall ? ctx->tmKVl[l] : ctx->tmKV;
     for (int wi = 0; wi < (int)ctx->waves.size(); ++wi) {
       const Wave& wv = ctx->waves[wi];
       const int n_w = wv.n_w;
@@ -449,7 +484,8 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
                            ctx->qoff, ctx->counts, ctx->kvsrc, ctx->reuse_ctr + l,
-                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s),
+                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s,
+                           (flags & RV_NO_COMPACTION) ? 1 : 0),
             "compact");
       const int* MC = ctx->counts;
       // a5: gather + LN1
@@ -463,7 +499,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out_ld = D;
         e.out_bf16 = 1;
         e.split = D;
-        e.out2 = ctx->KV;
+        e.out2 = KVl;
         e.out2_rows = ctx->idxC;
         e.out2_ld = 2LL * D;
         e.out2_bf16 = 1;
@@ -475,14 +511,14 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       {
         float* pcl = (!dense && l + 1 < L) ? ctx->pclsh : nullptr;
         if (!(flags & RV_ATTN_SYNC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM, T <= 257 (default)
-          r.chk(launch_attention_tc(ctx->tmQ, ctx->tmKV, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
+          r.chk(launch_attention_tc(ctx->tmQ, tmKVl, KVl, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
         else if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05/TMEM, any T (L/14@336)
-          r.chk(launch_attention_tcg(ctx->q, D, 0, 0, ctx->KV, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T,
-                                     D, H, s),
+          r.chk(launch_attention_tcg(ctx->q, D, 0, 0, KVl, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D,
+                                     H, s),
                 "attention");
         else   // mma.sync kernel: d_h = 16 (tiny config) or RV_ATTN_SYNC
-          r.chk(launch_attention(ctx->q, ctx->KV, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
+          r.chk(launch_attention(ctx->q, KVl, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
       }
       // a9: W_o + residual (gathered X_{l-1} rows)
@@ -551,7 +587,9 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   }
   // a14: Z = LN_post(CLS), slots are display indices
   r.begin(K_LNPOST,-1,-1);
-  r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
+  r.chk(launch_ln_post(keepall ? ctx->Xall + (size_t)L * nTD : ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T,
+                       D, s),
+        "ln_post");
 }
 
 // SPEC chain variant (RV_CHAIN; oracle/chain_ref.py):
@@ -984,7 +1022,9 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   for (int f = 0; f < n; ++f) nonI += (!dense && plan->type[f] != RV_I);
   const int total_desc = (int)ctx->wdesc_host.size() / 4;
   if (total_desc != n) return fail(ctx, RV_EPLAN, "rv_embed: internal wave bookkeeping mismatch");
-  if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w)))
+  const bool keepall = flags & RV_KEEP_ALL_CACHE;
+  if (keepall && (flags & RV_CHAIN)) return fail(ctx, RV_ECONTRACT, "rv_embed: RV_KEEP_ALL_CACHE is a D1-path ablation");
+  if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w, keepall)))
     return st;
   if (flags & RV_CHAIN) {
     if ((st = ensure_chain_buffers(ctx, n))) return st;
@@ -1137,8 +1177,8 @@ rv_status rv_wait(rv_ctx* ctx, rv_stats* stats) {
   stats->flops_exec = flops;
   stats->flops_dense = 2.0 * n * N * pp * D + (double)n * L * T * per_c;
   stats->bytes_alg = bytes;
-  const double cache = (double)n * T * (2 * D * 4 + 2 * D * 2);
-  stats->peak_cache_bytes = (uint64_t)cache;
+  stats->peak_cache_bytes = ctx->cache_bytes;      // allocated X + K/V cache of the mode used
+  stats->device_bytes = ctx->alloc_bytes;          // every per-embed device buffer
   stats->keepall_cache_bytes = (uint64_t)((double)n * T * ((L + 1) * D * 4 + L * 2 * D * 2));
   float ms = 0, msc = 0;
   cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);

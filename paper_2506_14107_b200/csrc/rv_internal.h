@@ -66,7 +66,8 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
                          int* cntR, bf16* dfull, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s);
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s,
+                           int all_c = 0);
 
 // 2D bf16 tensor map, box {64 cols, box_rows}, SWIZZLE_128B (k_gemm.cu)
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, int box_rows, char* err,

@@ -318,3 +318,55 @@ def test_empty_and_bad_inputs_fail_loudly(cuda_ok):
     x, c = synth.make_video(cfg, 4, 0.3, seed=1)
     with pytest.raises((ReuseViTError, ValueError)):
         m.embed(torch.from_numpy(x[:0]).cuda(), torch.from_numpy(c[:0]).cuda())
+
+
+@pytest.mark.parametrize("cfgname", ["b16", "l14_336"])
+def test_no_compaction_ablation_bitwise(cuda_ok, cfgname):
+    """RV_NO_COMPACTION (SURVEY §8(d) ablation step 1, masked dense: every token recomputed,
+    reused outputs overwritten by the restoration) gives the compacted path's embeddings and
+    masks bit for bit, at the dense path's executed work."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 21, 0.2, seed=44)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    Z1, M1, _, s1 = m.embed(xd, cd)
+    Z2, M2, _, s2 = m.embed(xd, cd, no_compaction=True)
+    torch.cuda.synchronize()
+    assert s1["reuse_all"] > 0.3
+    assert torch.equal(M1, M2) and torch.equal(Z1, Z2)
+    wc = m.wave_counts()
+    assert int(wc["M_C"].sum()) == 21 * cfg.layers * cfg.T     # every token recomputed
+
+
+def test_keep_all_cache_ablation(cuda_ok):
+    """RV_KEEP_ALL_CACHE (cached memory compaction off, Fig. 12 analogue): same
+    results bitwise with every layer's X and K/V kept; the allocated cache grows ~(L+1)/2x; at
+    the 7,200-frame L/14 workload it needs ~371 GB and fails cleanly with RV_ENOMEM, after which
+    the same context still embeds with the layer-wise cache (no dangling buffers)."""
+    from paper_2506_14107_b200._lib import ReuseViTError
+    cfg = synth.CONFIGS["b16"]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 41, 0.2, seed=45)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    Z1, M1, _, s1 = m.embed(xd, cd)
+    Z2, M2, _, s2 = m.embed(xd, cd, keep_all_cache=True)
+    torch.cuda.synchronize()
+    assert torch.equal(M1, M2) and torch.equal(Z1, Z2)
+    L, T, D, n = cfg.layers, cfg.T, cfg.dim, 41
+    assert s1["peak_cache_bytes"] == n * T * D * (2 * 4 + 2 * 2)
+    assert s2["peak_cache_bytes"] == n * T * D * ((L + 1) * 4 + L * 2 * 2)
+    assert s2["device_bytes"] > s1["device_bytes"]
+    # the bench workload: 7,200 frames of ViT-L/14
+    cfg = synth.CONFIGS["l14"]
+    m2, _, _ = build(cfg)
+    n = 7200
+    xb = torch.zeros((n, cfg.N, cfg.pp), dtype=torch.float32, device="cuda")
+    cb = torch.zeros((n, cfg.N), dtype=torch.float32, device="cuda")
+    with pytest.raises(ReuseViTError) as ei:
+        m2.embed(xb, cb, keep_all_cache=True, want_masks=False)
+    assert ei.value.status == -7          # RV_ENOMEM
+    del xb, cb
+    xs, cs = synth.make_video(cfg, 24, 0.2, seed=46)
+    Z3, _, _, s3 = m2.embed(torch.from_numpy(xs).cuda(), torch.from_numpy(cs).cuda())
+    torch.cuda.synchronize()
+    assert np.isfinite(Z3.cpu().numpy()).all() and s3["reuse_all"] > 0.3

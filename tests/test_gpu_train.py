@@ -107,55 +107,65 @@ def test_loss_and_gradient_parity(cuda_ok, R_target):
 
 
 def test_toy_training_meets_target_and_beats_random_reuse(cuda_ok):
-    """A toy run: 64 training groups, minibatches of 8, 150 Adam steps, temperature annealed
-    5 -> 0.1, R_target = 0.5, alpha = 2.  Checks: the loss falls; the hard-gated
-    inference path with the trained RVG1 blob reuses >= 0.35 of the tokens on held-out
-    video (the initial recompute-leaning gates reuse ~0); and its embeddings stay closer to
-    the dense ViT (1 - cos) than random reuse decisions at the same per-layer rate."""
+    """A toy run (tools/train_gates.py settings): a random ViT whose CLS embedding depends on
+    the frame content (init std 0.3), 256 training groups of 1-5-9-13-11-12 frames, minibatches
+    of 16, 300 Adam steps, temperature annealed 5 -> 0.1, R_target = 0.5, alpha = 2.
+    Checks: the loss falls below half its start; the hard-gated inference path (Eq. 4) with the
+    trained RVG1 blob reuses >= 0.35 of the non-I tokens of held-out video (the initial
+    recompute-leaning gates reuse none); its embeddings stay closer to the dense ViT (1 - cos)
+    than random reuse decisions at the same per-layer rate, and than reusing everything."""
     from paper_2506_14107_b200 import ReuseViT
-    W = synth.make_vit(CFG, random_ln=True)
+    W = synth.make_vit(CFG, random_ln=True, std=0.3)
     G0 = synth.init_train_gates(CFG)
     plan = oracle.group_plan()
-    pool, B, steps = 64, 8, 150
+    pool, B, steps = 256, 16, 300
     x, c = synth.make_train_groups(CFG, pool, plan["display"], seed=77)
+    xd, cd = _cuda(x), _cuda(c)
     t = _trainer(W, G0, plan, B, alpha=2.0, r_target=0.5, lr=3e-3)
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(78)
     logs = []
     for s in range(steps):
-        idx = rng.choice(pool, B, replace=False)
-        g = synth.make_gumbel((B, 6, CFG.layers, CFG.N, 2), seed=1000 + s)
-        logs.append(t.step(_cuda(x[idx]), _cuda(c[idx]), _cuda(g), tr.temperature(s, steps)))
+        idx = torch.from_numpy(rng.choice(pool, B, replace=False)).cuda()
+        g = synth.make_gumbel((B, 6, CFG.layers, CFG.N, 2), seed=10_000 + s)
+        logs.append(t.step(xd[idx].contiguous(), cd[idx].contiguous(), _cuda(g), tr.temperature(s, steps)))
     first = np.mean([l["l_total"] for l in logs[:10]])
     last = np.mean([l["l_total"] for l in logs[-10:]])
     print(f"train: l_total {first:.4f} -> {last:.4f}; last l_reuse {logs[-1]['l_reuse']:.3f} "
           f"l_sim {logs[-1]['l_sim']:.5f}")
     assert last < 0.5 * first
+    assert logs[-1]["l_reuse"] >= 0.45           # the hinge holds the soft reuse near R_target
     blob = t.gates()
     t.close()
     # hard-gated inference with the trained gates on a held-out 41-frame video
     m = ReuseViT(CFG, 0)
     m.load_vit(synth.pack_vit(CFG, W))
     m.load_gates(blob)
-    xv, cv = synth.make_video(CFG, 41, 0.15, seed=909)
+    xv, cv = synth.make_video(CFG, 41, 0.2, seed=909)
     Z, M, _, st = m.embed(_cuda(xv), _cuda(cv))
     Zd, _, _, _ = m.embed(_cuda(xv), _cuda(cv), dense=True)
     torch.cuda.synchronize()
     Mh = M.cpu().numpy()
     types = oracle.plan_gop(41)["type"]
-    reuse = Mh[types != 0].mean()
+    nonI = types != 0
+    reuse = Mh[nonI].mean()
     cos = lambda A, Bm: (A * Bm).sum(1) / np.linalg.norm(A, axis=1) / np.linalg.norm(Bm, axis=1)
-    Zn, Zdn = Z.cpu().numpy().astype(np.float64), Zd.cpu().numpy().astype(np.float64)
-    err_trained = float(np.mean(1 - cos(Zn, Zdn)))
-    # random decisions at the same per-layer rate (forced masks through the same path)
+    Zdn = Zd.cpu().numpy().astype(np.float64)
+    err = lambda Zx: float(np.mean(1 - cos(Zx.cpu().numpy().astype(np.float64), Zdn)))
+    err_trained = err(Z)
+    # random decisions at the same per-layer rate, and all-reuse (forced masks, same path)
     fm = np.zeros_like(Mh)
     rr = np.random.default_rng(6)
     for l in range(CFG.layers):
-        rate = Mh[types != 0, l].mean()
-        fm[types != 0, l] = (rr.random((int((types != 0).sum()), CFG.N)) < rate).astype(np.uint8)
+        rate = Mh[nonI, l].mean()
+        fm[nonI, l] = (rr.random((int(nonI.sum()), CFG.N)) < rate).astype(np.uint8)
     Zr, _, _, _ = m.embed(_cuda(xv), _cuda(cv), force_masks=torch.from_numpy(fm))
+    fa = np.zeros_like(Mh)
+    fa[nonI] = 1
+    Za, _, _, _ = m.embed(_cuda(xv), _cuda(cv), force_masks=torch.from_numpy(fa))
     torch.cuda.synchronize()
-    err_random = float(np.mean(1 - cos(Zr.cpu().numpy().astype(np.float64), Zdn)))
-    print(f"hard inference: reuse {reuse:.3f}  1-cos trained {err_trained:.2e}  random {err_random:.2e}")
+    err_random, err_all = err(Zr), err(Za)
+    print(f"hard inference: reuse {reuse:.3f}  1-cos trained {err_trained:.3e}  random {err_random:.3e}  "
+          f"all-reuse {err_all:.3e}")
     assert reuse >= 0.35
-    assert err_trained < err_random
+    assert err_trained < 0.75 * err_random and err_trained < err_all
     m.close()
