@@ -218,99 +218,88 @@ def run_reference(args):
             fh.write(json.dumps(line) + "\n")
 
 
-def run_c5(args):
+def setup_video(args, world, rank, dev):
+    """C4 (default: BASELINE configs[3], the 7,200-frame 1-hour L/14 video), and with --config /
+    --frames the C2 (B/16, 32 frames) and C3 (L/14, 256 frames) clips: one video sharded by
+    refresh group (+ right-edge halo I-frame) over the ranks."""
+    import synth
+    from paper_2506_14107_b200 import plan_gop
+    from paper_2506_14107_b200.dist import shard_frames as shard
+    cfg = synth.CONFIGS[args.config]
+    n_total = args.frames
+    f0, n_own, n_loc = shard(n_total, args.refresh, rank, world)
+    x_all, c_all = synth.make_video_torch(cfg, n_total, args.p, seed=2000, device=dev)
+    x = x_all[f0:f0 + n_loc].contiguous()
+    c = c_all[f0:f0 + n_loc].contiguous()
+    c[0] = 0.0                                   # slice starts at an I-frame
+    k = min(args.cpu_frames, n_total)
+    cpu = None
+    if rank == 0:                                # oracle sample: display frames 0..k-1 (prefix-closed)
+        cpu = {"x": x_all[:k].cpu().numpy(), "c": c_all[:k].cpu().numpy(), "plan_n": n_total, "rows": list(range(k)),
+               "sample": f"display frames 0-{k - 1} of the {n_total}-frame video (fp64 NumPy)"}
+    del x_all, c_all
+    names = {"l14": "CLIP ViT-L/14 224px", "b16": "CLIP ViT-B/16 224px", "l14_336": "CLIP ViT-L/14 336px",
+             "tiny": "tiny ViT"}
+    cfgname = names.get(args.config, args.config)
+    which = ("BASELINE configs[3]" if (args.config == "l14" and n_total == 7200) else
+             "BASELINE configs[1]" if (args.config == "b16" and n_total == 32) else
+             "BASELINE configs[2]" if (args.config == "l14" and n_total == 256) else "custom")
+    desc = (f"{cfgname} ReuseViT, {n_total}-frame video @2 FPS ({which}), motion p={args.p}, "
+            f"refresh {args.refresh}")
+    return {"cfg": cfg, "x": x, "c": c, "plan": plan_gop(n_loc, args.refresh), "n_emit": n_total, "n_loc": n_loc,
+            "n_own": n_own, "counts": [shard(n_total, args.refresh, r, world)[1] for r in range(world)],
+            "cpu": cpu, "desc": desc, "metric": METRIC if which == "BASELINE configs[3]" else
+            f"{cfgname} ReuseViT embedding frames/sec ({n_total}-frame video)",
+            "config_extra": {"frames": n_total, "frames_per_gpu": n_own, "halo_frames": n_loc - n_own,
+                             "parallelism": f"frame-group dp{world}",
+                             "l2": f"inputs {x.numel() * 4 / 1e9:.2f} GB fp32 per GPU"
+                                   + (" > 126 MB L2, no flush" if x.numel() * 4 > 126e6 else
+                                      "; kernels timed over a full embed (activations >> L2)")}}
+
+
+def setup_c5(args, world, rank, dev):
     """BASELINE configs[4] / SURVEY C5: ViT-L/14 336 px (T = 577) ReuseViT, 64 videos x 120
     frames (60-s clips at 2 FPS) with heterogeneous motion p in {.05, .1, .2, .4}; videos
     are assigned to the ranks by LPT on their estimated cost sum(1 - r_hat) and
-    each rank embeds its videos in ONE call (combined block-diagonal plan), then the
-    embeddings are all-gathered.  One step = embed + gather; max over ranks."""
+    each rank embeds its videos in ONE call (combined block-diagonal plan)."""
     import torch
-    import torch.distributed as dist
-
     import synth
-    from paper_2506_14107_b200 import ReuseViT, plan_gop
-    from paper_2506_14107_b200.dist import combine_plans, gather_rows, lpt_assign, max_over_ranks, reuse_estimate
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    from paper_2506_14107_b200 import plan_gop
+    from paper_2506_14107_b200.dist import combine_plans, lpt_assign, reuse_estimate
     cfg = synth.CONFIGS["l14_336"]
-    L, N, D = cfg.layers, cfg.N, cfg.dim
     ps = [(0.05, 0.1, 0.2, 0.4)[v % 4] for v in range(args.videos)]
-    costs = [args.video_frames * (1.0 - reuse_estimate(p, T=cfg.T, N=N)) for p in ps]
+    costs = [args.video_frames * (1.0 - reuse_estimate(p, T=cfg.T, N=cfg.N)) for p in ps]
     assign = lpt_assign(costs, world)
     mine = assign[rank]
     xs, cs = [], []
-    for v in mine:
-        x, c = synth.make_video_torch(cfg, args.video_frames, ps[v], seed=5000 + v, device=dev)
-        xs.append(x)
-        cs.append(c)
+    cpu = None
+    k = min(args.cpu_frames, args.video_frames)
+    for j, v in enumerate(mine):
+        xv, cv = synth.make_video_torch(cfg, args.video_frames, ps[v], seed=5000 + v, device=dev)
+        xs.append(xv)
+        cs.append(cv)
+        if j == 0 and rank == 0:                 # oracle sample: the first video's frames 0..k-1
+            cpu = {"x": xv[:k].cpu().numpy(), "c": cv[:k].cpu().numpy(), "plan_n": args.video_frames,
+                   "rows": list(range(k)),
+                   "sample": f"frames 0-{k - 1} of video {v} (p={ps[v]}, {args.video_frames} frames; fp64 NumPy)"}
     cp = combine_plans([plan_gop(args.video_frames, args.refresh) for _ in mine])
-    plan = {k: cp[k] for k in ("type", "past", "future", "order")}
     x = torch.cat(xs).contiguous()
     c = torch.cat(cs).contiguous()
     del xs, cs
-    n_loc = x.shape[0]
-    W = synth.make_vit(cfg)
-    G = synth.make_gates(cfg)
-    m = ReuseViT(cfg, local)
-    m.load_vit(synth.pack_vit(cfg, W))
-    m.load_gates(synth.pack_gates(cfg, G))
-    emb = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
-    masks = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    counts = [len(a) * args.video_frames for a in assign]
-
-    def step():
-        m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream)
-        st = m.wait()
-        if world > 1:
-            gather_rows([emb], counts)
-        return st
-
-    for _ in range(args.warmup):
-        st = step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        st = step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
     loads = [sum(costs[v] for v in a) for a in assign]
-    ms = max_over_ranks(ms)
     n_total = args.videos * args.video_frames
-    line = {"metric": "ViT-L/14@336 ReuseViT multi-video embedding frames/sec (64 videos x 120 frames)",
-            "value": n_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "CLIP ViT-L/14 336px (T=577) ReuseViT, 64 videos x 120 frames (BASELINE "
-                                   "configs[4]), per-video motion p in {.05,.1,.2,.4}, LPT sharding by estimated cost",
-                       "frames": n_total, "videos_per_gpu": [len(a) for a in assign],
-                       "est_load_per_gpu": [round(v, 1) for v in loads],
-                       "load_imbalance": max(loads) / (sum(loads) / world),
-                       "parallelism": f"video-group dp{world}", "seq_len": cfg.T},
-            "reuse": {"reuse_all": st["reuse_all"], "reuse_nonI": st["reuse_nonI"]},
-            "clocks": clk}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-        if args.out:
-            with open(args.out, "w") as fh:
-                fh.write(json.dumps(line) + "\n")
-    if world > 1:
-        dist.destroy_process_group()
+    return {"cfg": cfg, "x": x, "c": c, "plan": {kk: cp[kk] for kk in ("type", "past", "future", "order")},
+            "n_emit": n_total, "n_loc": x.shape[0], "n_own": x.shape[0],
+            "counts": [len(a) * args.video_frames for a in assign], "cpu": cpu,
+            "desc": f"CLIP ViT-L/14 336px (T=577) ReuseViT, {args.videos} videos x {args.video_frames} frames "
+                    "(BASELINE configs[4]), per-video motion p in {.05,.1,.2,.4}, LPT sharding by estimated cost",
+            "metric": f"ViT-L/14@336 ReuseViT multi-video embedding frames/sec ({args.videos} videos x "
+                      f"{args.video_frames} frames)",
+            "config_extra": {"frames": n_total, "videos_per_gpu": [len(a) for a in assign],
+                             "est_load_per_gpu": [round(v, 1) for v in loads],
+                             "load_imbalance": max(loads) / (sum(loads) / world),
+                             "parallelism": f"video-group dp{world}",
+                             "l2": f"inputs {x.numel() * 4 / 1e9:.2f} GB fp32 per GPU > 126 MB L2, no flush"}}
 
 
 def main():
@@ -318,16 +307,13 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
-    if args.workload == "c5":
-        run_c5(args)
-        return
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import synth
-    from paper_2506_14107_b200 import ReuseViT, plan_gop
-    from paper_2506_14107_b200.dist import gather_rows, max_over_ranks, shard_frames as shard
+    from paper_2506_14107_b200 import ReuseViT
+    from paper_2506_14107_b200.dist import gather_rows, max_over_ranks
     if os.environ.get("RV_LIB"):   # experiment builds (paper_2506_14107_b200.build.build_variant)
         from paper_2506_14107_b200 import _lib
         _lib.load_library(os.environ["RV_LIB"])
@@ -339,29 +325,19 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = synth.CONFIGS[args.config]
+    wl = setup_c5(args, world, rank, dev) if args.workload == "c5" else setup_video(args, world, rank, dev)
+    cfg, x, c, plan = wl["cfg"], wl["x"], wl["c"], wl["plan"]
     L, N, T, D = cfg.layers, cfg.N, cfg.T, cfg.dim
-    n_total = args.frames
-    f0, n_own, n_loc = shard(n_total, args.refresh, rank, world)
+    n_total, n_loc, counts = wl["n_emit"], wl["n_loc"], wl["counts"]
 
-    # ---- inputs: the same 7,200-frame video on every rank (seeded), this rank's slice
-    x_all, c_all = synth.make_video_torch(cfg, n_total, args.p, seed=2000, device=dev)
-    x = x_all[f0:f0 + n_loc].contiguous()
-    c = c_all[f0:f0 + n_loc].contiguous()
-    c[0] = 0.0                                   # slice starts at an I-frame
-    cpu_x = x_all[:args.cpu_frames].cpu().numpy() if rank == 0 else None
-    cpu_c = c_all[:args.cpu_frames].cpu().numpy() if rank == 0 else None
-    del x_all, c_all
     W = synth.make_vit(cfg)
     G = synth.make_gates(cfg)
     m = ReuseViT(cfg, local)
     m.load_vit(synth.pack_vit(cfg, W))
     m.load_gates(synth.pack_gates(cfg, G))
-    plan = plan_gop(n_loc, args.refresh)
     emb = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
     masks = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    counts = [shard(n_total, args.refresh, r, world)[1] for r in range(world)]
 
     def step(profile):
         m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync,
@@ -415,8 +391,6 @@ def main():
         h2d = int(xh.numel() * 4 + ch.numel() * 4)
         d2h = int(outs[0].size * 4 + outs[1].size)
 
-        max_ranks = max_over_ranks
-
         def hstep():
             m.embed_async(xh.numpy(), ch.numpy(), plan, out=outs, stream=stream)
             return m.wait()
@@ -430,7 +404,7 @@ def main():
             hstep()
         h1.record(stream)
         torch.cuda.synchronize()
-        ems_serial = max_ranks(h0.elapsed_time(h1) / args.steps)
+        ems_serial = max_over_ranks(h0.elapsed_time(h1) / args.steps)
 
         ems_pipe = None
         try:
@@ -457,7 +431,7 @@ def main():
             ss[0].wait_stream(ss[1])
             p1.record(ss[0])
             torch.cuda.synchronize()
-            ems_pipe = max_ranks(p0.elapsed_time(p1) / args.steps)
+            ems_pipe = max_over_ranks(p0.elapsed_time(p1) / args.steps)
             m2.close()
             del m2
         except RuntimeError as ex:      # e.g. not enough HBM for a second context
@@ -480,10 +454,11 @@ def main():
         d1.record(stream)
         torch.cuda.synchronize()
         own_dense = n_loc / (d0.elapsed_time(d1) / 1e3)
-        tdense = torch_dense_fps(cfg, W, x)
-        best = max(own_dense, tdense)
-        baselines = {"own_dense_fps": own_dense, "torch_dense_fps": tdense,
-                     "speedup_vs_best_dense": value / best}
+        tdense = {bs: torch_dense_fps(cfg, W, x, batch=bs) for bs in (64, 128, 256)}
+        best = max(own_dense, max(tdense.values()))
+        baselines = {"own_dense_fps": own_dense, "torch_dense_fps": max(tdense.values()),
+                     "torch_dense_fps_by_batch": tdense, "speedup_vs_best_dense": value / best,
+                     "speedup_vs_own_dense": value / own_dense}
 
     # ---- roofline of the dominant kernel class (timed inside the timed steps)
     peaks = measured_peaks()
@@ -531,31 +506,29 @@ def main():
     # ---- CPU oracle on a bounded sample + parity of the same frames
     cpu = None
     parity = None
-    if not args.no_cpu and rank == 0 and world == 1:
-        ref, dt, cores = oracle_sample(cfg, W, G, cpu_x, cpu_c, n_total, args.refresh, args.cpu_frames)
-        cpu = {"value": args.cpu_frames / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"display frames 0-{args.cpu_frames - 1} of the {n_total}-frame video (fp64 NumPy)"}
-        k = args.cpu_frames
-        Zg = emb[:k].double().cpu().numpy()
+    if not args.no_cpu and rank == 0 and world == 1 and wl["cpu"] is not None:
+        sm = wl["cpu"]
+        ref, dt, cores = oracle_sample(cfg, W, G, sm["x"], sm["c"], sm["plan_n"], args.refresh, len(sm["rows"]))
+        k = len(sm["rows"])
+        cpu = {"value": k / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sm["sample"]}
+        Zg = emb[sm["rows"]].double().cpu().numpy()
         Zr = ref["Z"][:k]
         err = np.abs(Zg - Zr).max(1) / np.abs(Zr).max(1)
         cos = (Zg * Zr).sum(1) / np.linalg.norm(Zg, axis=1) / np.linalg.norm(Zr, axis=1)
         d = ref["d"][:k]
         band = ~np.isnan(d) & (np.abs(np.nan_to_num(d)) >= 1e-3)
-        agree = float((masks[:k].cpu().numpy() == ref["M"][:k])[band].mean()) if band.any() else 1.0
+        agree = float((masks[sm["rows"]].cpu().numpy() == ref["M"][:k])[band].mean()) if band.any() else 1.0
         parity = {"frames": k, "max_rel_err": float(err.max()), "min_cos": float(cos.min()),
                   "mask_agree": agree, "tol": {"max_rel_err": 2e-2, "min_cos": 0.999, "mask_agree": 0.999}}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": wl["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"CLIP ViT-L/14 224px ReuseViT, {n_total}-frame 1-hour video @2 FPS "
-                                   f"(BASELINE configs[3]), motion p={args.p}, refresh {args.refresh}",
-                       "model": "ViT-L/14 (random init) + structured gates", "frames": n_total,
-                       "frames_per_gpu": n_own, "halo_frames": n_loc - n_own, "seq_len": T,
-                       "parallelism": f"frame-group dp{world}", "l2": "inputs 4.3 GB fp32 > 126 MB L2, no flush",
+            "config": {"workload": wl["desc"], "model": f"{args.config if args.workload != 'c5' else 'l14_336'} "
+                                                        "(random init) + structured gates",
+                       "seq_len": T, **wl["config_extra"],
                        "compute": "bf16 operands, fp32 accumulate, fp32 residual",
                        "variant": "SPEC chain (RV_CHAIN)" if args.chain else "D1 layer-gated (default)"},
             "reuse": {"reuse_all": stats["reuse_all"], "reuse_nonI": stats["reuse_nonI"]},
@@ -567,7 +540,8 @@ def main():
             "roofline": roof, "kernels": kernels, "profiled_ms_sum": step_ms_prof,
             "e2e": e2e, "gpu_launches": int(stats["n_launches"]) * args.steps,
             "clocks": clk, "baselines": baselines, "cpu_baseline": cpu, "parity": parity,
-            "cache_bytes": {"layerwise": stats["peak_cache_bytes"], "keep_all_layers": stats["keepall_cache_bytes"]},
+            "cache_bytes": {"layerwise": stats["peak_cache_bytes"], "keep_all_layers": stats["keepall_cache_bytes"],
+                            "device_bytes": stats["device_bytes"]},
         }
         s = json.dumps(line)
         print(s, flush=True)
