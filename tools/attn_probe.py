@@ -16,7 +16,8 @@ def main():
     ap.add_argument("--frames", type=int, default=288)
     ap.add_argument("--nq", type=int, default=57)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--only", default="both", choices=["both", "tc", "sync"])
+    ap.add_argument("--only", default="both", choices=["both", "tc", "sync", "tcg", "all"])
+    ap.add_argument("--config", default="l14")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -24,7 +25,7 @@ def main():
     from paper_2506_14107_b200 import ReuseViT, _lib
     if os.environ.get("RV_LIB"):   # experiment build (paper_2506_14107_b200.build.build_variant)
         _lib.load_library(os.environ["RV_LIB"])
-    cfg = synth.CONFIGS["l14"]
+    cfg = synth.CONFIGS[a.config]
     T, D, H = cfg.T, cfg.dim, cfg.heads
     m = ReuseViT(cfg, 0)
     m.load_vit(synth.pack_vit(cfg, synth.make_vit(cfg)))
@@ -41,7 +42,8 @@ def main():
     pcls = torch.zeros(n_w, H, cfg.N, device="cuda")
     st = torch.cuda.current_stream()
     flops = 4.0 * float(qoff[-1]) * T * D
-    for use_tc in ([False, True] if a.only == "both" else [a.only == "tc"]):
+    modes = {"both": [0, 1], "tc": [1], "sync": [0], "tcg": [2], "all": [0, 1, 2]}[a.only]
+    for use_tc in modes:
         for _ in range(3):
             m.stage_attention(wdesc, qo, q, KV, out, pcls, st, use_tc=use_tc)
         torch.cuda.synchronize()
@@ -52,7 +54,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
-        print(f"{'tcgen05' if use_tc else 'mma.sync'}: {ms * 1e3:.1f} us/launch, {flops / ms / 1e9:.1f} TFLOP/s, "
+        print(f"{['mma.sync', 'tcgen05', 'tcgen05-general'][use_tc]}: {ms * 1e3:.1f} us/launch, {flops / ms / 1e9:.1f} TFLOP/s, "
               f"K/V {n_w * T * 2 * D * 2 / ms / 1e6:.0f} GB/s")
 
 

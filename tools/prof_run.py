@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--p", type=float, default=0.2)
     ap.add_argument("--iters", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--counts-out", default=None, help="write the per-wave M_C / M_R counts (JSON)")
     a = ap.parse_args()
     import torch
     import synth
@@ -32,6 +33,13 @@ def main():
         Z, M, _, st = m.embed(xd, cd, graph=not a.no_graph)
     torch.cuda.synchronize()
     print({k: st[k] for k in ("reuse_all", "ms_compute", "n_launches")})
+    if a.counts_out:
+        import json
+        wc = m.wave_counts()
+        with open(a.counts_out, "w") as fh:
+            json.dump({"frames": wc["frames"].tolist(), "M_C": wc["M_C"].tolist(), "M_R": wc["M_R"].tolist(),
+                       "config": a.config, "n": a.frames, "p": a.p, "T": cfg.T, "D": cfg.dim, "F": cfg.ffn,
+                       "Hr": cfg.hidden_r}, fh)
 
 
 if __name__ == "__main__":

@@ -12,8 +12,10 @@ dense (RV_DENSE) and over a torch cuBLAS + SDPA dense ViT, and parity of the fir
 
 Ablation ladder at p = 0.4 (~61% reuse, the paper's Fig. `fig:eval-ablation` point,
 P:709-713), each step adding one mechanism:
-  1. masked dense         every token computed (RV_DENSE: what hard gating costs without
-                          skipping work; selecting the reused outputs is free)
+  0. dense ViT            RV_DENSE: every token recomputed, no gates (the reference speed)
+  1. masked dense         RV_NO_COMPACTION: hard gating decides, every token is still computed
+                          and the reused tokens' outputs are replaced by the restoration (the
+                          paper's "hard gating alone", P:711)
   2. per-frame compaction each frame compacted on its own (RV_WAVE_FRAME: one wave per frame)
   3. level-batched        cross-frame compaction of a level's frames, one 20-frame refresh group
                           (+ its right-edge I frame) resident at a time (no cached memory
@@ -42,7 +44,7 @@ def main():
     ap.add_argument("--ablation-p", type=float, default=0.4)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--parity-frames", type=int, default=9)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep_r1.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "sweep_r2.json"))
     a = ap.parse_args()
 
     import numpy as np
@@ -128,6 +130,7 @@ def main():
     o_ab = outs(n_ab)
     ms_dense_ab, _ = timed(lambda: m.embed(x, c, dense=True, out=o_ab))
     ms_full, (_, _, _, st) = timed(lambda: m.embed(x, c, out=o_ab))
+    ms_masked, _ = timed(lambda: m.embed(x, c, no_compaction=True, out=o_ab))
     ms_frame, _ = timed(lambda: m.embed(x, c, per_frame_waves=True, out=o_ab))
     xb, cb, o_g = torch.empty_like(x[:21]), torch.empty_like(c[:21]), outs(21)
 
@@ -141,10 +144,11 @@ def main():
     halo = k_groups * 21 - n_ab
     ms_dense = ms_dense_ab
     n = n_ab
-    ladder = [("masked dense (RV_DENSE)", ms_dense), ("per-frame compaction (RV_WAVE_FRAME)", ms_frame),
+    ladder = [("dense ViT (RV_DENSE)", ms_dense), ("masked dense: hard gating, no compaction (RV_NO_COMPACTION)", ms_masked),
+              ("per-frame compaction (RV_WAVE_FRAME)", ms_frame),
               ("level-batched, one refresh group resident", ms_group), ("all groups resident (default)", ms_full)]
     doc["ablation"] = {"p": p, "frames": n_ab, "reuse_all": st["reuse_all"], "halo_frames_step3": halo,
-                       "steps": [{"step": k + 1, "name": nm, "ms": v, "fps": n / (v / 1e3), "speedup": ms_dense / v}
+                       "steps": [{"step": k, "name": nm, "ms": v, "fps": n / (v / 1e3), "speedup": ms_dense / v}
                                  for k, (nm, v) in enumerate(ladder)],
                        "paper": {"hard gating": 1.25, "+ sparse compaction": 1.45, "+ memory compaction": 1.62,
                                  "cite": "P:709-713, at 61% reuse, RTX 3090"}}
