@@ -780,287 +780,9 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
 }
 
 
-// ============================================================================================
-// attn_tcg_kernel — the general-shape tcgen05 attention (any T <= 1024 with d_h = 64): CLIP
-// L/14@336 (T = 577, BASELINE configs[4]) and the SPEC chain variant's dense attention (every
-// token a query, q read from the q|k|v cache through the source-row table; SURVEY §8(f)
-// NEXT-1).  One CTA per (frame, head, 128-query tile), two CTAs per SM:
-//   warp 0     loader: gathers the tile's 128 query rows and, per 128-key block, the K and V
-//              rows (through `kvsrc`: the reuse cache read in place, a7) with cp.async into
-//              SWIZZLE_128B tiles of a 2-stage ring; completion on mbarriers (arrive.noinc)
-//   warp 1     TMEM allocator + one MMA-issuing lane: per key block S = Q K^T (M = 128,
-//              N = 128, 4 K-steps), then, once the softmax has stored P, O += P V (8 MMAs,
-//              P read from TMEM); MMAs of one thread execute in issue order, so S of block
-//              kb + 1 overwrites P of block kb only after P V(kb) has read it
-//   warps 2-5  softmax, one query row per thread (TMEM lane = row): online softmax over the
-//              key blocks in the log2 domain with lazy rescaling (the running max moves only
-//              when a block's max exceeds it by more than 8, i.e. P <= 2^8; then O in TMEM
-//              is rescaled, warp-uniformly); epilogue O / l -> bf16; the CLS query row also
-//              writes its normalised probabilities over the patch keys (feature t).
-// TMEM (256 columns): S / P at [0, 128) (P packed bf16 over [0, 64)), O at [128, 192).
-constexpr int AG_THREADS = 192;
-constexpr int AG_ROWS = 128;                    // query rows per tile (= MMA M)
-constexpr int AG_KB = 128;                      // keys per block (= S MMA N)
-constexpr int AG_NS = 2;                        // K/V ring stages
-constexpr uint32_t AG_TILE = AG_ROWS * 128;     // 128 rows x 128 B
-constexpr uint32_t AG_Q = 0;
-constexpr uint32_t AG_RING = AG_TILE;           // stage s: K at RING + 2 s TILE, V at + TILE
-constexpr uint32_t AG_BAR = AG_RING + 2 * AG_NS * AG_TILE;
-constexpr uint32_t AG_SMEM = AG_BAR + 256 + 1024;   // + barriers, + 1 KB alignment slack
-constexpr int AG_MAXKB = 8;                     // T <= 1024
-
-RV_DEV void tld32x32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-RV_DEV void tst32x32(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-
-// q_mode 0: query rows q[qoff[w] + r] (compacted, ld D); 1: every token of the frame is a query,
-// its q row = q_src[kvsrc[slot T + i]] at column q_col (cache-resident q, chain variant)
-__global__ void __launch_bounds__(AG_THREADS, 2)
-    attn_tcg_kernel(const bf16* __restrict__ qbuf, long long q_ld, int q_col, int q_mode, const bf16* __restrict__ KV,
-                    long long kv_ld, const int* __restrict__ kvsrc, bf16* __restrict__ out,
-                    const int4* __restrict__ wdesc, const int* __restrict__ qoff, float* __restrict__ pclsh,
-                    int n_w, int T, int D, int H, int n_qt, float scale_log2) {
-  extern __shared__ __align__(1024) uint8_t sm_raw[];
-  // 1 KB alignment for the SWIZZLE_128B atoms
-  uint8_t* sm = sm_raw + ((1024 - (su32(sm_raw) & 1023)) & 1023);
-  const uint32_t base = su32(sm);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + AG_BAR);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + AG_NS, *s_full = kv_empty + AG_NS,
-           *p_full = s_full + 1, *o_full = p_full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_full + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // item = (w, h, qt), qt fastest: the tiles of one frame-head run side by side (L2 reuse)
-  const long long item = blockIdx.x;
-  const int qt = (int)(item % n_qt);
-  const int h = (int)((item / n_qt) % H);
-  const int w = (int)(item / ((long long)n_qt * H));
-  const int a = __ldg(qoff + w), nq = __ldg(qoff + w + 1) - a;
-  const int q0 = qt * AG_ROWS;
-  if (q0 >= nq) return;                       // dead tile (fewer queries in this frame)
-  const int nrows = min(AG_ROWS, nq - q0);
-  const int slot = __ldg(&wdesc[w].x);
-  const int nkb = (T + AG_KB - 1) / AG_KB;
-  const long long srow0 = (long long)slot * T;
-  if (tid == 0) {
-    mbar_init(q_full, 32);
-    for (int i = 0; i < AG_NS; ++i) {
-      mbar_init(&kv_full[i], 32);
-      mbar_init(&kv_empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = *tslot;
-  if (warp == 0) {
-    // ------------------------------------------------------------------ loader
-    const int c = lane & 7;                   // 16 B chunk of a 128 B row
-    {
-      const uint32_t dst = base + AG_Q;
-      for (int rb = 0; rb < AG_ROWS; rb += 4) {
-        const int r = rb + (lane >> 3);
-        long long src;
-        if (q_mode == 0) src = (long long)(a + q0 + min(r, nrows - 1)) * q_ld;
-        else src = (long long)__ldg(kvsrc + srow0 + q0 + min(r, nrows - 1)) * q_ld;
-        cp_async16(dst + (uint32_t)r * 128 + ((c ^ (r & 7)) << 4), qbuf + src + q_col + h * 64 + c * 8);
-      }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(q_full)) : "memory");
-    }
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % AG_NS;
-      mbar_wait(&kv_empty[s], ((kb / AG_NS) & 1) ^ 1);
-      const uint32_t dk = base + AG_RING + (uint32_t)(2 * s) * AG_TILE, dv = dk + AG_TILE;
-      for (int rb = 0; rb < AG_KB; rb += 4) {
-        const int r = rb + (lane >> 3);
-        const int j = kb * AG_KB + r;
-        // keys past T read the frame's CLS row (finite data, masked in the softmax)
-        const long long row = j < T ? (kvsrc ? (long long)__ldg(kvsrc + srow0 + j) : srow0 + j) : srow0;
-        const bf16* src = KV + row * kv_ld + h * 64 + c * 8;
-        const uint32_t off = (uint32_t)r * 128 + ((c ^ (r & 7)) << 4);
-        cp_async16(dk + off, src);
-        cp_async16(dv + off, src + D);
-      }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&kv_full[s])) : "memory");
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc64(AG_KB, 0, AG_ROWS), id_o = idesc64(64, 1, AG_ROWS);
-      const uint32_t tS = tmem, tO = tmem + 128;
-      mbar_wait(q_full, 0);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % AG_NS;
-        const uint32_t sk = base + AG_RING + (uint32_t)(2 * s) * AG_TILE, sv = sk + AG_TILE;
-        mbar_wait(&kv_full[s], (kb / AG_NS) & 1);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
-        tc_after();
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mma_ss(tS, sdesc(base + AG_Q + k * 32), sdesc(sk + k * 32), id_s, k != 0);
-        mma_commit(s_full);
-        mbar_wait(p_full, kb & 1);             // P (and any O rescale) stored by the softmax warps
-        tc_after();
-#pragma unroll
-        for (int k = 0; k < AG_KB / 16; ++k)
-          mma_ts(tO, tS + (uint32_t)(k * 8), sdesc(sv + (uint32_t)k * 2048), id_o, (kb | k) != 0);
-        mma_commit(&kv_empty[s]);
-      }
-      mma_commit(o_full);
-    }
-  } else {
-    // ------------------------------------------------------------------ softmax + epilogue
-    const int qd = warp & 3;                   // TMEM lane quarter of this warp
-    const int row = qd * 32 + lane;            // query row of the tile
-    const uint32_t lrow = (uint32_t)(qd * 32) << 16;
-    const uint32_t tS = tmem + lrow, tO = tmem + lrow + 128;
-    const bool cls_row = pclsh && (q_mode == 1 ? (q0 + row == 0) : (q0 + row == 0)) && row < nrows;
-    float* prow = cls_row ? pclsh + ((long long)slot * H + h) * (T - 1) : nullptr;
-    float m_run = -INFINITY, l = 0.f;
-    float mblk[AG_MAXKB];
-    for (int kb = 0; kb < nkb; ++kb) {
-      mbar_wait(s_full, kb & 1);
-      tc_after();
-      float v[AG_KB];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) tld32x32(tS + 32 * i, v + 32 * i);
-      tld_wait();
-      const int kv0 = kb * AG_KB;
-      float bm = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < AG_KB; ++i) {
-        v[i] = kv0 + i < T ? v[i] * scale_log2 : -INFINITY;
-        bm = fmaxf(bm, v[i]);
-      }
-      // lazy rescale: move the running max only when this block would push P above 2^8
-      const bool need = kb == 0 || bm > m_run + 8.f;
-      const float m_new = need ? fmaxf(bm, m_run) : m_run;
-      if (kb > 0 && __any_sync(0xffffffffu, need)) {
-        // O holds sum over blocks < kb: complete, since S(kb) completed after P V(kb - 1)
-        const float f = ex2f_fast(m_run - m_new);
-#pragma unroll 1
-        for (int hc = 0; hc < 2; ++hc) {
-          float o[32];
-          tld32x32(tO + 32 * hc, o);
-          tld_wait();
-          uint32_t u[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(o[i] * f);
-          tst32x32(tO + 32 * hc, u);
-        }
-        l *= f;
-      }
-      m_run = m_new;
-      if (kb < AG_MAXKB) mblk[kb] = m_run;
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < AG_KB; ++i) {
-        v[i] = ex2f_fast(v[i] - m_run);
-        sum += v[i];
-      }
-      l += sum;
-      if (cls_row) {                            // unnormalised, fixed up after the last block
-#pragma unroll
-        for (int i = 0; i < AG_KB; ++i) {
-          const int j = kv0 + i;
-          if (j >= 1 && j < T) prow[j - 1] = v[i];
-        }
-      }
-      uint32_t pk[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-      tst32x32(tS, pk);
-      tst32x32(tS + 32, pk + 32);
-      tst_wait();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    mbar_wait(o_full, 0);
-    tc_after();
-    float o[64];
-    tld32x32(tO, o);
-    tld32x32(tO + 32, o + 32);
-    tld_wait();
-    if (row < nrows) {
-      const float il = 1.f / l;
-      bf16* dst = out + (long long)(a + q0 + row) * D + h * 64;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 u;
-        u.x = pack_bf16x2(o[8 * c] * il, o[8 * c + 1] * il);
-        u.y = pack_bf16x2(o[8 * c + 2] * il, o[8 * c + 3] * il);
-        u.z = pack_bf16x2(o[8 * c + 4] * il, o[8 * c + 5] * il);
-        u.w = pack_bf16x2(o[8 * c + 6] * il, o[8 * c + 7] * il);
-        *reinterpret_cast<uint4*>(dst + 8 * c) = u;
-      }
-    }
-    if (cls_row) {
-      const float il = 1.f / l;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const float f = ex2f_fast(mblk[kb] - m_run) * il;
-        for (int i = 0; i < AG_KB; ++i) {
-          const int j = kb * AG_KB + i;
-          if (j >= 1 && j < T) prow[j - 1] *= f;
-        }
-      }
-    }
-  }
-  tc_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
-  }
-}
-
 }  // namespace
 
 bool attn_tc_supported(int T, int D, int H) { return H > 0 && D % H == 0 && D / H == 64 && T >= 2 && T - 1 <= A8_MAXK; }
-bool attn_tcg_supported(int T, int D, int H) { return H > 0 && D % H == 0 && D / H == 64 && T >= 2 && T <= AG_KB * AG_MAXKB; }
-
-cudaError_t launch_attention_tcg(const bf16* q, long long q_ld, int q_col, int q_mode, const bf16* KV, long long kv_ld,
-                                 const int* kvsrc, bf16* out, const int* wdesc, const int* qoff, float* pclsh, int n_w,
-                                 int T, int D, int H, cudaStream_t s) {
-  if (n_w <= 0) return cudaSuccess;
-  if (!attn_tcg_supported(T, D, H)) return cudaErrorInvalidValue;
-  cudaError_t e = ensure_smem<attn_tcg_kernel>(AG_SMEM);
-  if (e != cudaSuccess) return e;
-  const int n_qt = (T + AG_ROWS - 1) / AG_ROWS;     // a frame has at most T queries
-  const long long grid = (long long)n_w * H * n_qt;
-  const float scale_log2 = 1.4426950408889634f / 8.0f;   // 1/sqrt(64) * log2(e)
-  attn_tcg_kernel<<<(unsigned)grid, AG_THREADS, AG_SMEM, s>>>(q, q_ld, q_col, q_mode, KV, kv_ld, kvsrc, out,
-                                                              reinterpret_cast<const int4*>(wdesc), qoff, pclsh, n_w, T,
-                                                              D, H, n_qt, scale_log2);
-  return cudaGetLastError();
-}
-
 size_t attn_tc_smem() { return A8_META + A8_NQ * sizeof(Meta) + (2 * A8_NQ + 2 * A8_NT + 16) * 8 + 16; }
 
 cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const bf16* KV, const int* kvsrc,

@@ -514,7 +514,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
           r.chk(launch_attention_tc(ctx->tmQ, tmKVl, KVl, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
                 "attention");
         else if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05/TMEM, any T (L/14@336)
-          r.chk(launch_attention_tcg(ctx->q, D, 0, 0, KVl, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D,
+          r.chk(launch_attention_tcg(&ctx->tmQ, ctx->q, D, 0, 0, KVl, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D,
                                      H, s),
                 "attention");
         else   // mma.sync kernel: d_h = 16 (tiny config) or RV_ATTN_SYNC
@@ -663,7 +663,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       r.begin(K_ATTN,l,wi);
       float* pcl_chain = (!dense && l + 1 < L) ? P[l & 1] : nullptr;
       if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05: q from the cache via the table
-        r.chk(launch_attention_tcg(Qc, ld3, 2 * D, 1, Qc, ld3, KS[l & 1], ctx->att, wd, ctx->qoffT, pcl_chain, n_w, T, D,
+        r.chk(launch_attention_tcg(nullptr, Qc, ld3, 2 * D, 1, Qc, ld3, KS[l & 1], ctx->att, wd, ctx->qoffT, pcl_chain, n_w, T, D,
                                    H, s),
               "attention");
       else
@@ -1361,9 +1361,12 @@ rv_status rv_stage_attention(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, con
   CK(cudaSetDevice(ctx->device));
   if (use_tc == 2 || (use_tc == 1 && !attn_tc_supported(ctx->T, ctx->D, ctx->H))) {   // general tcgen05 kernel
     if (!attn_tcg_supported(ctx->T, ctx->D, ctx->H))
-      return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and T <= 1024");
-    CK(launch_attention_tcg((const bf16*)q, ctx->D, 0, 0, (const bf16*)KV, 2LL * ctx->D, kvsrc, (bf16*)out, wdesc, qoff,
-                            pcls, n_w, ctx->T, ctx->D, ctx->H, (cudaStream_t)stream));
+      return fail(ctx, RV_ECONTRACT, "rv_stage_attention: tcgen05 attention needs d_h = 64 and T <= 1025");
+    CUtensorMap tm;
+    char e[256];
+    if (!make_tmap_bf16(&tm, q, q_rows, ctx->D, 64, e, sizeof e)) return fail(ctx, RV_ECUDA, "%s", e);
+    CK(launch_attention_tcg(&tm, (const bf16*)q, ctx->D, 0, 0, (const bf16*)KV, 2LL * ctx->D, kvsrc, (bf16*)out, wdesc,
+                            qoff, pcls, n_w, ctx->T, ctx->D, ctx->H, (cudaStream_t)stream));
     return RV_OK;
   }
   if (use_tc) {

@@ -79,14 +79,15 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV,
                                 bf16* out,
                                 const int* wdesc, const int* qoff, float* pclsh, int n_w, int T, int D, int H,
                                 cudaStream_t s);
-// general-shape tcgen05 attention (k_attn_tc.cu attn_tcg_kernel): d_h = 64, T <= 1024.
-// q_mode 0: compacted queries q[qoff[w] + r] (row stride q_ld); 1: every token of a frame is a
-// query with its q row q[kvsrc[slot T + i]] at column q_col (chain variant's q|k|v cache);
-// K / V rows through kvsrc with stride kv_ld (K at column h d_h, V at D + h d_h)
+// general-shape tcgen05 attention (k_attn_tcg.cu): d_h = 64, T - 1 <= 1024.
+// q_mode 0: compacted queries q[qoff[w] + r], loaded through tmQ (box {64, 64} over q, row stride
+// q_ld = D); 1: every token of a frame is a query with its q row q[kvsrc[slot T + i]] at column
+// q_col (chain variant's q|k|v cache, tmQ unused); K / V rows through kvsrc (identity if null)
+// with stride kv_ld (K at column h d_h, V at D + h d_h); output rows qoff[w] + r.
 bool attn_tcg_supported(int T, int D, int H);
-cudaError_t launch_attention_tcg(const bf16* q, long long q_ld, int q_col, int q_mode, const bf16* KV, long long kv_ld,
-                                 const int* kvsrc, bf16* out, const int* wdesc, const int* qoff, float* pclsh, int n_w,
-                                 int T, int D, int H, cudaStream_t s);
+cudaError_t launch_attention_tcg(const CUtensorMap* tmQ, const bf16* q, long long q_ld, int q_col, int q_mode,
+                                 const bf16* KV, long long kv_ld, const int* kvsrc, bf16* out, const int* wdesc,
+                                 const int* qoff, float* pclsh, int n_w, int T, int D, int H, cudaStream_t s);
 // kv_ld: K/V cache row stride (0 -> 2D); q_cache: queries are all T tokens of each frame with q read
 // from the cache row at column 2D through kvsrc (SPEC chain variant), qoff[w] = w*T
 cudaError_t launch_attention(const bf16* q, const bf16* KV, const int* kvsrc, bf16* out, const int* wdesc,
