@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(256) patch_to_bf16_rows_kernel(const float* __
 
 cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP,
                                  cudaStream_t s) {
-  if (pp % 4 == 0 && KP % 4 == 0) {   // vectorised path (all CLIP shapes: pp = 3 p^2 with even p)
+  // vectorised path (all CLIP shapes: pp = 3 p^2 with even p) needs 16 B aligned rows: a caller's
+  // view with a storage offset that is not a multiple of 4 floats takes the scalar kernel
+  if (pp % 4 == 0 && KP % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
     long long g = (rows + 7) / 8;
     if (g > 148 * 16) g = 148 * 16;
     patch_to_bf16_rows_kernel<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(src, dst, rows, pp, KP);

@@ -1260,6 +1260,13 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
       MC = log[((size_t)r.l * nwv + r.w) * 2];
       MR = log[((size_t)r.l * nwv + r.w) * 2 + 1];
       nw = ctx->waves[r.w].n_w;
+      if (ctx->cur_flags & RV_CHAIN) {
+        // SPEC chain variant: attention and W_o run over every token; LN1 + QKV of layer l + 1
+        // (tagged l + 1) are gated by layer l's decision, layer 1's run over every token
+        if (r.cls == K_ATTN || r.cls == K_WO) MC = nw * T;
+        if (r.cls == K_GATHER || r.cls == K_QKV)
+          MC = r.l == 0 ? nw * T : log[((size_t)(r.l - 1) * nwv + r.w) * 2];
+      }
     }
     // Algorithmic FLOPs (tensor work) and HBM bytes of this launch.
     switch (r.cls) {

@@ -51,7 +51,7 @@ CASES = [
     ("b16", 32, 32, 0.3, "bimodal"),
     ("b16", 32, 32, 0.1, "bimodal"),
     ("l14", 64, 21, 0.2, "bimodal"),
-    ("l14_336", 24, 9, 0.2, "bimodal"),          # C5 shape: T = 577 (mma.sync attention)
+    ("l14_336", 24, 9, 0.2, "bimodal"),          # C5 shape: T = 577 (general tcgen05 attention)
     ("b16", 32, 32, 0.3, "bimodal", "sync"),
     ("l14", 64, 21, 0.2, "bimodal", "sync"),
 ]
@@ -181,6 +181,23 @@ def test_determinism_graph_and_host_paths(cuda_ok):
     assert torch.equal(Z1, Z3) and torch.equal(M1, M3)
     assert np.array_equal(Z1.cpu().numpy(), Z4) and np.array_equal(M1.cpu().numpy(), M4)
     assert st["ms_total"] > 0 and st["n_launches"] > 0
+
+
+def test_misaligned_device_patches(cuda_ok):
+    """A contiguous patch view whose storage offset is not a multiple of 4 floats (not 16 B
+    aligned) takes the scalar conversion kernel and gives the bitwise same embedding."""
+    cfg = synth.CONFIGS["b16"]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, 6, 0.3, seed=19)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    buf = torch.empty(xd.numel() + 1, device="cuda")
+    buf[1:] = xd.flatten()
+    xm = buf[1:].view(xd.shape)
+    assert xm.is_contiguous() and xm.data_ptr() % 16 != 0
+    Z1, M1, _, _ = m.embed(xd, cd)
+    Z2, M2, _, _ = m.embed(xm, cd)
+    torch.cuda.synchronize()
+    assert torch.equal(Z1, Z2) and torch.equal(M1, M2)
 
 
 @pytest.mark.parametrize("cfgname,n,n_check,p", [("tiny", 12, 12, 0.3), ("b16", 24, 24, 0.3), ("l14", 32, 9, 0.2)])
