@@ -89,6 +89,8 @@ typedef struct {
   int32_t n_launches;         /* kernels launched by the last embed (own kernels only)          */
   float reuse_by_layer[64];   /* per-layer Eq. 14 reuse rate over non-I frames                  */
   uint64_t device_bytes;      /* bytes of every per-embed device buffer the context allocated   */
+  int32_t wave_ring;          /* wavefront schedule: ring size R of the layer buffers (X_l in
+                                 slot l % R); 0 = serial level waves (see RV_SERIAL_WAVES)        */
 } rv_stats;
 
 /* rv_embed flags */
@@ -111,6 +113,11 @@ typedef struct {
 #define RV_KEEP_ALL_CACHE 512u /* ablation of cached memory compaction (Fig. 12
                               analogue): keep every layer's X and K/V allocated; at the 7,200-frame
                               workload this needs ~371 GB and fails with RV_ENOMEM               */
+#define RV_SERIAL_WAVES 1024u /* run the level waves strictly one after another (layer by layer).
+                              Default: when every wave holds <= 512 frames, wave (l, k) starts as
+                              soon as wave (l, k-1) and wave (l-1, k) are done (wavefront over
+                              rings of R layer buffers, one stream per wave index);
+                              results are bitwise identical, only the concurrency differs        */
 #define RV_ATTN_SYNC 32u   /* diagnostic: attention on the mma.sync kernel (k_attn.cu) even where the
                               tcgen05/TMEM kernels (k_attn_tc.cu: d_h = 64) apply; without it the
                               mma.sync kernel runs only for d_h = 16 (the tiny config)            */

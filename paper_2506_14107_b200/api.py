@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (RV_ATTN_SYNC, RV_CHAIN, RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_KEEP_ALL_CACHE,
-                   RV_NO_COMPACTION, RV_NO_GRAPH, RV_PROFILE, RV_WAVE_FRAME, RvConfig, RvKernelProf, RvPlan, RvStats,
+                   RV_NO_COMPACTION, RV_NO_GRAPH, RV_PROFILE, RV_SERIAL_WAVES, RV_WAVE_FRAME, RvConfig, RvKernelProf, RvPlan, RvStats,
                    check, load_library)
 
 __all__ = ["ReuseViT", "plan_gop", "plan_check", "vit_blob_floats", "gate_blob_floats"]
@@ -118,7 +118,7 @@ class ReuseViT:
                     want_scores: bool = False, stream=None, graph: bool = True, out=None,
                     profile: bool = False, attn_tc: bool = True,
                     per_frame_waves: bool = False, chain: bool = False, no_compaction: bool = False,
-                    keep_all_cache: bool = False):
+                    keep_all_cache: bool = False, serial_waves: bool = False):
         """Enqueue one embed; returns a handle for ``wait``.  ``out`` optionally supplies the
         output buffers (emb, masks, scores) to reuse across calls (same pointers -> the
         cached CUDA graph is replayed)."""
@@ -132,7 +132,8 @@ class ReuseViT:
         flags = ((RV_DENSE if dense else 0) | (0 if graph else RV_NO_GRAPH) | (RV_PROFILE if profile else 0)
                  | (0 if attn_tc else RV_ATTN_SYNC)
                  | (RV_WAVE_FRAME if per_frame_waves else 0) | (RV_CHAIN if chain else 0)
-                 | (RV_NO_COMPACTION if no_compaction else 0) | (RV_KEEP_ALL_CACHE if keep_all_cache else 0))
+                 | (RV_NO_COMPACTION if no_compaction else 0) | (RV_KEEP_ALL_CACHE if keep_all_cache else 0)
+                 | (RV_SERIAL_WAVES if serial_waves else 0))
         if force_masks is not None:
             flags |= RV_FORCE_MASKS
         if device_path:
@@ -179,7 +180,7 @@ class ReuseViT:
                 "peak_cache_bytes": int(s.peak_cache_bytes), "keepall_cache_bytes": int(s.keepall_cache_bytes),
                 "ms_total": s.ms_total, "ms_compute": s.ms_compute, "n_levels": s.n_levels,
                 "n_launches": s.n_launches, "reuse_by_layer": list(s.reuse_by_layer[:L]),
-                "device_bytes": int(s.device_bytes)}
+                "device_bytes": int(s.device_bytes), "wave_ring": int(s.wave_ring)}
 
     def wave_counts(self) -> dict:
         """Level-wave structure of the last embed (after ``wait``): frames per wave and the

@@ -46,7 +46,24 @@ struct Wave {
   bool any_ref;  // at least one frame with a decision (non-I, not dense)
 };
 
+// Scratch of one level-wave (decision outputs, compaction maps, GEMM operands).  The serial
+// schedule shares one set (the rv_ctx fields); the wavefront schedule gives every wave its own
+// set, sized by its frames, with the A-operand tensor maps of its GEMMs (maps != false).
+struct WaveBuf {
+  uint8_t *wmask = nullptr, *wprov = nullptr;
+  int *cntR = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr,
+      *rpos = nullptr;
+  bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *hr = nullptr, *dfull = nullptr;
+  float* x1 = nullptr;
+  bool maps = false;
+  CUtensorMap tmQ, tmA, tmAtt, tmH, tmD, tmHr;   // q {64 x 64}; GEMM A operands {64 x 128}
+};
+
 thread_local std::string g_create_err;
+
+// Level waves of at most this many frames may use the wavefront schedule; larger waves fill the
+// GPU on their own (the 7,200-frame workload's 360-1,440-frame waves run serially).
+constexpr int kWavefrontMaxWave = 512;
 
 }  // namespace
 
@@ -106,6 +123,23 @@ struct rv_ctx {
   CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
   CUtensorMap tmKV;                // K/V cache [n T][2 D], box {64, 1}: row gathers (tcgen05 attention)
   std::vector<GemmPlan> g_qkv, g_wo, g_fc1, g_fc2, g_r1, g_r2;
+  // ---- wavefront schedule (level waves too small to fill the GPU): wave (l, k)
+  // runs as soon as wave (l, k-1) (its references) and wave (l-1, k) (its input) are done, on
+  // one stream per wave index, so waves of different layers overlap along the diagonals.  X_l
+  // lives in a ring of R layer buffers (Xr[l % R]), K/V_l and the source-row table in rings of
+  // R - 1; wave (l, k) waits for wave (l-R+1, last) before overwriting a ring slot.
+  int wf_R = 0;                        // ring size of the current embed (0: serial level waves)
+  std::vector<long long> wf_key;       // (n_cap, R, wave sizes) the allocations below were made for
+  std::vector<void*> wfallocs;
+  std::vector<float*> Xr;              // [R]: Xr[0], Xr[1] alias X[0], X[1]
+  std::vector<bf16*> KVr;              // [R-1]: KVr[0] aliases KV
+  std::vector<int*> KSr;               // [R-1]: KSr[0] aliases kvsrc
+  std::vector<CUtensorMap> tmKVr;
+  std::vector<WaveBuf> wbuf;           // per wave; wbuf[0] points at the shared buffers
+  std::vector<cudaStream_t> wstreams;  // one per wave index
+  std::vector<cudaEvent_t> wevents;    // [L][waves] completion of wave (l, k)
+  cudaEvent_t wf_fork = nullptr;
+  unsigned long long wf_bytes = 0, wf_cache_bytes = 0;
   // ---- graph cache
   cudaGraphExec_t gexec = nullptr;
   std::vector<long long> gkey;
@@ -273,7 +307,16 @@ rv_status check_plan(rv_ctx* ctx, const rv_plan* p, std::vector<int>* level_out)
 // Drop every per-embed buffer and the state encoded from their addresses (graph, tensor maps,
 // GEMM plans): after a failed re-allocation the context holds no dangling pointer, and the
 // next embed allocates again from scratch.
+void release_wavefront(rv_ctx* ctx) {
+  if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+  free_list(ctx->wfallocs);
+  ctx->wf_key.clear();
+  ctx->Xr.clear(); ctx->KVr.clear(); ctx->KSr.clear(); ctx->tmKVr.clear(); ctx->wbuf.clear();
+  ctx->wf_bytes = ctx->wf_cache_bytes = 0;
+}
+
 void release_buffers(rv_ctx* ctx) {
+  release_wavefront(ctx);   // its rings alias X[0], X[1], KV and kvsrc
   if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
   free_list(ctx->ballocs);
   ctx->n_cap = 0; ctx->capC = 0; ctx->capR = 0; ctx->wdesc_cap = 0; ctx->chain_cap = 0;
@@ -381,6 +424,114 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   return RV_OK;
 }
 
+// Bytes the wavefront schedule adds for ring size R on top of ensure_buffers' allocations.
+unsigned long long wavefront_bytes(const rv_ctx* ctx, int n, int R, const std::vector<Wave>& waves) {
+  const unsigned long long T = ctx->T, D = ctx->D, N = ctx->N, F = ctx->F, Hr = ctx->Hr;
+  unsigned long long b = (unsigned long long)(R - 2) * n * T * D * 4 + (unsigned long long)(R - 2) * n * T * (2 * D * 2 + 4);
+  for (size_t wi = 1; wi < waves.size(); ++wi) {
+    const unsigned long long rows = waves[wi].n_w * T, capC = (rows + 127) / 128 * 128;
+    const unsigned long long capR = std::max<unsigned long long>(128, (waves[wi].n_w * N + 127) / 128 * 128);
+    b += rows * (2 + 4 + D * 2) + capC * (4 + D * 2 * 3 + D * 4 + F * 2) + capR * (8 + Hr * 2) + waves[wi].n_w * 8 + 64;
+  }
+  return b;
+}
+
+// Wavefront buffers for ring size R >= 3: the extra X / K/V / source-row ring slots and every
+// wave's own scratch (wave 0 keeps the shared set).  Streams and events persist in the context.
+rv_status ensure_wavefront(rv_ctx* ctx, int R) {
+  const int nw = (int)ctx->waves.size(), L = ctx->L;
+  std::vector<long long> key = {(long long)ctx->n_cap, (long long)R, ctx->capC, ctx->capR};
+  for (const Wave& w : ctx->waves) key.push_back(w.n_w * 2 + (w.any_ref ? 1 : 0));
+  if (key == ctx->wf_key) return RV_OK;
+  release_wavefront(ctx);
+  const long long n = ctx->n_cap, T = ctx->T, D = ctx->D, N = ctx->N;
+  auto& B = ctx->wfallocs;
+  rv_status s;
+  unsigned long long bytes = 0, cache = 0;
+#define AL(ptr, cnt)                                                                  \
+  if ((s = dalloc(ctx, B, &ptr, (size_t)(cnt)))) { release_wavefront(ctx); return s; } \
+  bytes += (unsigned long long)(cnt) * sizeof(*ptr)
+  ctx->Xr.assign(R, nullptr);
+  ctx->Xr[0] = ctx->X[0];
+  ctx->Xr[1] = ctx->X[1];
+  for (int r = 2; r < R; ++r) { AL(ctx->Xr[r], n * T * D); }
+  ctx->KVr.assign(R - 1, nullptr);
+  ctx->KSr.assign(R - 1, nullptr);
+  ctx->KVr[0] = ctx->KV;
+  ctx->KSr[0] = ctx->kvsrc;
+  for (int r = 1; r < R - 1; ++r) {
+    AL(ctx->KVr[r], n * T * 2 * D);
+    AL(ctx->KSr[r], n * T);
+  }
+  cache = bytes;
+  char e[256];
+  bool ok = true;
+  ctx->tmKVr.resize(R - 1);
+  for (int r = 0; ok && r < R - 1; ++r) ok = make_tmap_bf16(&ctx->tmKVr[r], ctx->KVr[r], n * T, 2 * (int)D, 1, e, sizeof e);
+  ctx->wbuf.assign(nw, WaveBuf());
+  for (int wi = 0; ok && wi < nw; ++wi) {
+    WaveBuf& b = ctx->wbuf[wi];
+    const long long nwf = ctx->waves[wi].n_w;
+    long long capC = ctx->capC, capR = ctx->capR, rowsD = (long long)ctx->wdesc_cap * T;
+    if (wi == 0) {
+      b.wmask = ctx->wmask; b.wprov = ctx->wprov; b.cntR = ctx->cntR; b.idxC = ctx->idxC; b.idxR = ctx->idxR;
+      b.provrow = ctx->provrow; b.qoff = ctx->qoff; b.counts = ctx->counts; b.rpos = ctx->rpos; b.A = ctx->A;
+      b.q = ctx->q; b.att = ctx->att; b.h = ctx->h; b.hr = ctx->hr; b.dfull = ctx->dfull; b.x1 = ctx->x1;
+    } else {
+      capC = (nwf * T + 127) / 128 * 128;
+      capR = std::max<long long>(128, (nwf * N + 127) / 128 * 128);
+      rowsD = nwf * T;
+      AL(b.wmask, nwf * T);
+      AL(b.wprov, nwf * T);
+      AL(b.cntR, nwf);
+      AL(b.qoff, nwf + 1);
+      AL(b.counts, 2);
+      AL(b.rpos, nwf * T);
+      AL(b.idxC, capC);
+      AL(b.idxR, capR);
+      AL(b.provrow, capR);
+      AL(b.A, capC * D);
+      AL(b.q, capC * D);
+      AL(b.att, capC * D);
+      AL(b.x1, capC * D);
+      AL(b.h, capC * ctx->F);
+      AL(b.hr, capR * ctx->Hr);
+      AL(b.dfull, rowsD * D);
+      if (cudaMemset(b.dfull, 0, (size_t)rowsD * D * sizeof(bf16)) != cudaSuccess) {
+        release_wavefront(ctx);
+        return fail(ctx, RV_ECUDA, "cudaMemset failed");
+      }
+    }
+    b.maps = true;
+    ok = make_tmap_bf16(&b.tmQ, b.q, capC, (int)D, 64, e, sizeof e) &&
+         make_tmap_bf16(&b.tmA, b.A, capC, (int)D, 128, e, sizeof e) &&
+         make_tmap_bf16(&b.tmAtt, b.att, capC, (int)D, 128, e, sizeof e) &&
+         make_tmap_bf16(&b.tmH, b.h, capC, ctx->F, 128, e, sizeof e) &&
+         make_tmap_bf16(&b.tmD, b.dfull, rowsD, (int)D, 128, e, sizeof e) &&
+         make_tmap_bf16(&b.tmHr, b.hr, capR, ctx->Hr, 128, e, sizeof e);
+  }
+#undef AL
+  if (!ok) {
+    release_wavefront(ctx);
+    return fail(ctx, RV_ECUDA, "%s", e);
+  }
+  while ((int)ctx->wstreams.size() < nw) {
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ctx->wstreams.push_back(st);
+  }
+  while ((int)ctx->wevents.size() < L * nw) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->wevents.push_back(ev);
+  }
+  if (!ctx->wf_fork) CK(cudaEventCreateWithFlags(&ctx->wf_fork, cudaEventDisableTiming));
+  ctx->wf_key = key;
+  ctx->wf_bytes = bytes;
+  ctx->wf_cache_bytes = cache;
+  return RV_OK;
+}
+
 // Staging buffers of host-pointer embeds (never allocated on the RV_DEVICE_PTRS path).
 rv_status ensure_host_buffers(rv_ctx* ctx, int n, bool scores) {
   rv_status s;
@@ -442,6 +593,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
                   float* emb, uint8_t* masks, float* scores) {
   const int L = ctx->L, D = ctx->D, T = ctx->T, N = ctx->N, H = ctx->H, F = ctx->F, Hr = ctx->Hr;
   cudaStream_t s = r.s;
+  const cudaStream_t s0 = s;   // the embed stream (wave streams fork from and join into it)
   const bool dense = flags & RV_DENSE;
   const bool force = flags & RV_FORCE_MASKS;
   r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
@@ -463,100 +615,146 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         "embed_finish");
   const bool keepall = ctx->keepall;
   const size_t nTD = (size_t)ctx->n_cap * T * D;
+  const int R = ctx->wf_R;                 // >= 3: wavefront schedule over rings of layer buffers
+  const int nwv = (int)ctx->waves.size();
+  // X_l (input of layer l + 1), K/V_l and the source-row table of layer l
+  auto Xbuf = [&](int l) -> float* {
+    return keepall ? ctx->Xall + (size_t)l * nTD : (R ? ctx->Xr[l % R] : ctx->X[l & 1]);
+  };
+  auto KVbuf = [&](int l) -> bf16* {
+    return keepall ? ctx->KVall + (size_t)l * 2 * nTD : (R ? ctx->KVr[l % (R - 1)] : ctx->KV);
+  };
+  auto tmKVbuf = [&](int l) -> const CUtensorMap& {
+    return keepall ? ctx->tmKVl[l] : (R ? ctx->tmKVr[l % (R - 1)] : ctx->tmKV);
+  };
+  auto KSbuf = [&](int l) -> int* { return R ? ctx->KSr[l % (R - 1)] : ctx->kvsrc; };
+  WaveBuf shared;   // the serial schedule's wave buffers (tensor maps: the GEMM plans' own)
+  shared.wmask = ctx->wmask; shared.wprov = ctx->wprov; shared.cntR = ctx->cntR; shared.idxC = ctx->idxC;
+  shared.idxR = ctx->idxR; shared.provrow = ctx->provrow; shared.qoff = ctx->qoff; shared.counts = ctx->counts;
+  shared.rpos = ctx->rpos; shared.A = ctx->A; shared.q = ctx->q; shared.att = ctx->att; shared.h = ctx->h;
+  shared.hr = ctx->hr; shared.dfull = ctx->dfull; shared.x1 = ctx->x1;
+  auto plan = [](const GemmPlan& p, const WaveBuf& b, const CUtensorMap& a) {
+    GemmPlan q = p;
+    if (b.maps) q.tmA = a;
+    return q;
+  };
+  if (R) {   // fork: every wave stream starts after the patch embed
+    r.chk(cudaEventRecord(ctx->wf_fork, s), "fork");
+    --r.launches;
+    for (int wi = 0; wi < nwv; ++wi) {
+      r.chk(cudaStreamWaitEvent(ctx->wstreams[wi], ctx->wf_fork, 0), "fork");
+      --r.launches;
+    }
+  }
   for (int l = 0; l < L; ++l) {
     const LayerW& w = ctx->lw[l];
-    float* Xin = keepall ? ctx->Xall + (size_t)l * nTD : ctx->X[l & 1];
-    float* Xout = keepall ? ctx->Xall + (size_t)(l + 1) * nTD : ctx->X[(l + 1) & 1];
-    bf16* KVl = keepall ? ctx->KVall + (size_t)l * 2 * nTD : ctx->KV;
-    const CUtensorMap& tmKVl = keepall ? ctx->tmKVl[l] : ctx->tmKV;
-    for (int wi = 0; wi < (int)ctx->waves.size(); ++wi) {
+    float* Xin = Xbuf(l);
+    float* Xout = Xbuf(l + 1);
+    bf16* KVl = KVbuf(l);
+    const CUtensorMap& tmKVl = tmKVbuf(l);
+    int* kvsrc = KSbuf(l);
+    for (int wi = 0; wi < nwv; ++wi) {
       const Wave& wv = ctx->waves[wi];
       const int n_w = wv.n_w;
       const int* wd = ctx->wdesc + (size_t)wv.off * 4;
       const int maxC = n_w * T;
+      const WaveBuf& b = R ? ctx->wbuf[wi] : shared;
+      if (R) {
+        // wave (l, wi) runs after wave (l, wi - 1) (the lower levels hold its references) and,
+        // since it overwrites ring slots, after wave (l - R + 1, last): the last reader of
+        // X_{l-R} (scores of layer l - R + 1) and of K/V_{l-R+1} and its source rows.  Wave
+        // (l - 1, wi) precedes it on its own stream.
+        s = ctx->wstreams[wi];
+        r.s = s;
+        if (wi > 0) {
+          r.chk(cudaStreamWaitEvent(s, ctx->wevents[(size_t)l * nwv + wi - 1], 0), "wave dependency");
+          --r.launches;
+        }
+        if (l - R + 1 >= 0) {
+          r.chk(cudaStreamWaitEvent(s, ctx->wevents[(size_t)(l - R + 1) * nwv + nwv - 1], 0), "ring dependency");
+          --r.launches;
+        }
+      }
       // a2-a3: Eq. 1-4
       r.begin(K_SCORE,l,wi);
       r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
-                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
-                         ctx->wprov, ctx->cntR, ctx->dfull, s),
+                         ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, b.wmask,
+                         b.wprov, b.cntR, b.dfull, s),
             "score");
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
-      r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
-                           ctx->qoff, ctx->counts, ctx->kvsrc, ctx->reuse_ctr + l,
-                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s,
+      r.chk(launch_compact(n_w, T, wd, b.wmask, b.wprov, b.cntR, b.idxC, b.idxR, b.provrow, b.qoff, b.counts, kvsrc,
+                           ctx->reuse_ctr + l, ctx->count_log + ((size_t)l * nwv + wi) * 2, b.rpos, s,
                            (flags & RV_NO_COMPACTION) ? 1 : 0),
             "compact");
-      const int* MC = ctx->counts;
+      const int* MC = b.counts;
       // a5: gather + LN1
       r.begin(K_GATHER,l,wi);
-      r.chk(launch_gather_ln(Xin, ctx->idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, ctx->A, D, s), "gather_ln1");
+      r.chk(launch_gather_ln(Xin, b.idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, b.A, D, s), "gather_ln1");
       // a6: QKV; q compact, K/V scattered to the cache rows of C
       {
         Epi e;
         e.bias = w.bqkv;
-        e.out = ctx->q;
+        e.out = b.q;
         e.out_ld = D;
         e.out_bf16 = 1;
         e.split = D;
         e.out2 = KVl;
-        e.out2_rows = ctx->idxC;
+        e.out2_rows = b.idxC;
         e.out2_ld = 2LL * D;
         e.out2_bf16 = 1;
         r.begin(K_QKV,l,wi);
-        r.chk(gemm_launch(ctx->g_qkv[l], MC, 0, maxC, e, s), "gemm_qkv");
+        r.chk(gemm_launch(plan(ctx->g_qkv[l], b, b.tmA), MC, 0, maxC, e, s), "gemm_qkv");
       }
       // a8: attention over all T keys; CLS row -> t for layer l+1
       r.begin(K_ATTN,l,wi);
       {
         float* pcl = (!dense && l + 1 < L) ? ctx->pclsh : nullptr;
+        const CUtensorMap& tmQ = b.maps ? b.tmQ : ctx->tmQ;
         if (!(flags & RV_ATTN_SYNC) && attn_tc_supported(T, D, H))   // tcgen05/TMEM, T <= 257 (default)
-          r.chk(launch_attention_tc(ctx->tmQ, tmKVl, KVl, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
-                "attention");
+          r.chk(launch_attention_tc(tmQ, tmKVl, KVl, kvsrc, b.att, wd, b.qoff, pcl, n_w, T, D, H, s), "attention");
         else if (!(flags & RV_ATTN_SYNC) && attn_tcg_supported(T, D, H))   // tcgen05/TMEM, any T (L/14@336)
-          r.chk(launch_attention_tcg(&ctx->tmQ, ctx->q, D, 0, 0, KVl, 2LL * D, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D,
-                                     H, s),
+          r.chk(launch_attention_tcg(&tmQ, b.q, D, 0, 0, KVl, 2LL * D, kvsrc, b.att, wd, b.qoff, pcl, n_w, T, D, H, s),
                 "attention");
         else   // mma.sync kernel: d_h = 16 (tiny config) or RV_ATTN_SYNC
-          r.chk(launch_attention(ctx->q, KVl, ctx->kvsrc, ctx->att, wd, ctx->qoff, pcl, n_w, T, D, H, s),
-                "attention");
+          r.chk(launch_attention(b.q, KVl, kvsrc, b.att, wd, b.qoff, pcl, n_w, T, D, H, s), "attention");
       }
       // a9: W_o + residual (gathered X_{l-1} rows)
       {
         Epi e;
         e.bias = w.bo;
         e.resid = Xin;
-        e.resid_rows = ctx->idxC;
+        e.resid_rows = b.idxC;
         e.resid_ld = D;
-        e.out = ctx->x1;
+        e.out = b.x1;
         e.out_ld = D;
         r.begin(K_WO,l,wi);
-        r.chk(gemm_launch(ctx->g_wo[l], MC, 0, maxC, e, s), "gemm_wo");
+        r.chk(gemm_launch(plan(ctx->g_wo[l], b, b.tmAtt), MC, 0, maxC, e, s), "gemm_wo");
       }
       // a10: LN2 + FC1 + QuickGELU
       r.begin(K_LN2,l,wi);
-      r.chk(launch_gather_ln(ctx->x1, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
+      r.chk(launch_gather_ln(b.x1, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, b.A, D, s), "ln2");
       {
         Epi e;
         e.bias = w.b1;
         e.act = 1;
-        e.out = ctx->h;
+        e.out = b.h;
         e.out_ld = F;
         e.out_bf16 = 1;
         r.begin(K_FC1,l,wi);
-        r.chk(gemm_launch(ctx->g_fc1[l], MC, 0, maxC, e, s), "gemm_fc1");
+        r.chk(gemm_launch(plan(ctx->g_fc1[l], b, b.tmA), MC, 0, maxC, e, s), "gemm_fc1");
       }
       // a11: FC2 + residual, scattered to X_l rows of C (Eq. 10, C side)
       {
         Epi e;
         e.bias = w.b2;
-        e.resid = ctx->x1;
+        e.resid = b.x1;
         e.resid_ld = D;
         e.out = Xout;
-        e.out_rows = ctx->idxC;
+        e.out_rows = b.idxC;
         e.out_ld = D;
         r.begin(K_FC2,l,wi);
-        r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
+        r.chk(gemm_launch(plan(ctx->g_fc2[l], b, b.tmH), MC, 0, maxC, e, s), "gemm_fc2");
       }
       // a12: restoration (Eq. 9) + merge (Eq. 10, R side).  The score pass wrote Delta (Eq. 8)
       // into the wave-local token rows w*T+i; R1 reads them in place over all n_w*T rows and
@@ -566,30 +764,39 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;
-        e1.out = ctx->hr;
+        e1.out = b.hr;
         e1.out_ld = Hr;
         e1.out_bf16 = 1;
-        e1.out_rows = ctx->rpos;
+        e1.out_rows = b.rpos;
         r.begin(K_R1,l,wi);
-        r.chk(gemm_launch(ctx->g_r1[l], nullptr, n_w * T, n_w * T, e1, s), "gemm_r1");
+        r.chk(gemm_launch(plan(ctx->g_r1[l], b, b.tmD), nullptr, n_w * T, n_w * T, e1, s), "gemm_r1");
         Epi e2;
         e2.bias = w.br2;
         e2.resid = Xout;
-        e2.resid_rows = ctx->provrow;
+        e2.resid_rows = b.provrow;
         e2.resid_ld = D;
         e2.out = Xout;
-        e2.out_rows = ctx->idxR;
+        e2.out_rows = b.idxR;
         e2.out_ld = D;
         r.begin(K_R2,l,wi);
-        r.chk(gemm_launch(ctx->g_r2[l], ctx->counts + 1, 0, n_w * N, e2, s), "gemm_r2");
+        r.chk(gemm_launch(plan(ctx->g_r2[l], b, b.tmHr), b.counts + 1, 0, n_w * N, e2, s), "gemm_r2");
       }
+      if (R) {
+        r.chk(cudaEventRecord(ctx->wevents[(size_t)l * nwv + wi], s), "wave event");
+        --r.launches;
+      }
+    }
+  }
+  if (R) {   // join every wave stream back into the embed stream
+    s = r.s = s0;
+    for (int wi = 0; wi < nwv; ++wi) {
+      r.chk(cudaStreamWaitEvent(s, ctx->wevents[(size_t)(L - 1) * nwv + wi], 0), "join");
+      --r.launches;
     }
   }
   // a14: Z = LN_post(CLS), slots are display indices
   r.begin(K_LNPOST,-1,-1);
-  r.chk(launch_ln_post(keepall ? ctx->Xall + (size_t)L * nTD : ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T,
-                       D, s),
-        "ln_post");
+  r.chk(launch_ln_post(Xbuf(L), ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
 }
 
 // SPEC chain variant (RV_CHAIN; oracle/chain_ref.py):
@@ -1026,6 +1233,28 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   if (keepall && (flags & RV_CHAIN)) return fail(ctx, RV_ECONTRACT, "rv_embed: RV_KEEP_ALL_CACHE is a D1-path ablation");
   if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w, keepall)))
     return st;
+  // Wavefront schedule when the level waves are too small to fill the GPU and the
+  // rings fit: the largest R <= min(L + 1, waves + 1) whose extra bytes stay within half of the
+  // free device memory (the rest is left to the caller, e.g. a second pipelined context).
+  // Profiled, ablation and chain embeds keep the serial level order.
+  ctx->wf_R = 0;
+  if (!(flags & (RV_SERIAL_WAVES | RV_PROFILE | RV_KEEP_ALL_CACHE | RV_CHAIN | RV_WAVE_FRAME)) &&
+      ctx->waves.size() >= 2 && max_w <= kWavefrontMaxWave) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const unsigned long long avail = fr + ctx->wf_bytes, reserve = 4ull << 30;
+    const unsigned long long budget = avail > reserve ? (avail - reserve) / 2 : 0;
+    int R = std::min(L + 1, (int)ctx->waves.size() + 1);
+    while (R >= 3 && wavefront_bytes(ctx, ctx->n_cap, R, ctx->waves) > budget) --R;
+    if (R >= 3) {
+      if (ensure_wavefront(ctx, R) == RV_OK) {
+        ctx->wf_R = R;
+      } else {   // could not allocate the rings: the serial schedule needs nothing more
+        release_wavefront(ctx);
+        ctx->err.clear();
+      }
+    }
+  }
   if (flags & RV_CHAIN) {
     if ((st = ensure_chain_buffers(ctx, n))) return st;
     const int nd = (int)ctx->wdesc_host.size() / 4;
@@ -1050,8 +1279,6 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   ctx->prof_valid = false;
   cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : nullptr;
   const bool devp = flags & RV_DEVICE_PTRS;
-  if (devp && ((uintptr_t)patches & 15))
-    return fail(ctx, RV_ECONTRACT, "rv_embed: device patches must be 16-byte aligned (vectorised loads)");
   if (!devp && (st = ensure_host_buffers(ctx, n, scores != nullptr))) return st;
   const float* d_patches = devp ? patches : ctx->in_patches;
   const float* d_codec = devp ? codec : ctx->in_codec;
@@ -1088,7 +1315,7 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   std::vector<long long> key = {(long long)n, (long long)(flags & ~RV_NO_GRAPH), (long long)(intptr_t)d_patches,
                                 (long long)(intptr_t)d_codec, (long long)(intptr_t)d_emb,
                                 (long long)(intptr_t)d_masks, (long long)(intptr_t)d_scores,
-                                (long long)(intptr_t)ws, ctx->capC, ctx->capR};
+                                (long long)(intptr_t)ws, ctx->capC, ctx->capR, (long long)ctx->wf_R};
   for (int v : ctx->wdesc_host) key.push_back(v);
   Rec rec{ctx, ws};
   rec.prof = (flags & RV_PROFILE) != 0;
@@ -1177,8 +1404,10 @@ rv_status rv_wait(rv_ctx* ctx, rv_stats* stats) {
   stats->flops_exec = flops;
   stats->flops_dense = 2.0 * n * N * pp * D + (double)n * L * T * per_c;
   stats->bytes_alg = bytes;
-  stats->peak_cache_bytes = ctx->cache_bytes;      // allocated X + K/V cache of the mode used
-  stats->device_bytes = ctx->alloc_bytes;          // every per-embed device buffer
+  const bool wf = ctx->wf_R >= 3;                  // wavefront rings and per-wave scratch in use
+  stats->peak_cache_bytes = ctx->cache_bytes + (wf ? ctx->wf_cache_bytes : 0);   // X + K/V cache of the mode used
+  stats->device_bytes = ctx->alloc_bytes + (wf ? ctx->wf_bytes : 0);            // every per-embed device buffer
+  stats->wave_ring = ctx->wf_R;
   stats->keepall_cache_bytes = (uint64_t)((double)n * T * ((L + 1) * D * 4 + L * 2 * D * 2));
   float ms = 0, msc = 0;
   cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
@@ -1200,6 +1429,10 @@ void rv_destroy(rv_ctx* ctx) {
   free_list(ctx->hsallocs);
   free_list(ctx->wallocs);
   if (ctx->count_log) cudaFree(ctx->count_log);
+  free_list(ctx->wfallocs);
+  for (auto st : ctx->wstreams) cudaStreamDestroy(st);
+  for (auto e : ctx->wevents) cudaEventDestroy(e);
+  if (ctx->wf_fork) cudaEventDestroy(ctx->wf_fork);
   for (auto e : ctx->prof_pool) cudaEventDestroy(e);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

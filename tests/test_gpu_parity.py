@@ -183,6 +183,27 @@ def test_determinism_graph_and_host_paths(cuda_ok):
     assert st["ms_total"] > 0 and st["n_launches"] > 0
 
 
+@pytest.mark.parametrize("cfgname,n,p", [("tiny", 41, 0.2), ("b16", 32, 0.3), ("l14", 64, 0.2), ("l14_336", 24, 0.2)])
+def test_wavefront_equals_serial_waves(cuda_ok, cfgname, n, p):
+    """Wavefront schedule (default for small level waves: wave (l, k) overlaps waves of other
+    layers, X / K/V / source rows in rings of R layers, per-wave scratch) vs RV_SERIAL_WAVES:
+    the same kernels on the same rows, so the embeddings, masks and scores are bitwise equal;
+    with and without the CUDA graph."""
+    cfg = synth.CONFIGS[cfgname]
+    m, W, G = build(cfg)
+    x, c = synth.make_video(cfg, n, p, seed=3100 + n)
+    xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
+    Z0, M0, S0, st0 = m.embed(xd, cd, want_scores=True, serial_waves=True)
+    Z1, M1, S1, st1 = m.embed(xd, cd, want_scores=True)
+    Z2, M2, S2, st2 = m.embed(xd, cd, want_scores=True, graph=False)
+    torch.cuda.synchronize()
+    assert st0["wave_ring"] == 0 and st1["wave_ring"] >= 3 and st2["wave_ring"] == st1["wave_ring"]
+    assert st1["device_bytes"] > st0["device_bytes"]
+    for Z, M, S in ((Z1, M1, S1), (Z2, M2, S2)):
+        assert torch.equal(Z0, Z) and torch.equal(M0, M)
+        assert torch.equal(torch.nan_to_num(S0, nan=-7.0), torch.nan_to_num(S, nan=-7.0))
+
+
 def test_misaligned_device_patches(cuda_ok):
     """A contiguous patch view whose storage offset is not a multiple of 4 floats (not 16 B
     aligned) takes the scalar conversion kernel and gives the bitwise same embedding."""

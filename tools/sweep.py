@@ -100,8 +100,10 @@ def main():
     for p in [float(v) for v in a.ps.split(",")]:
         x, c = synth.make_video_torch(cfg, n, p, seed=2000 + n)
         ms, (Z, M, _, st) = timed(lambda: m.embed(x, c, out=o_n))
+        ms_ser, _ = timed(lambda: m.embed(x, c, out=o_n, serial_waves=True))
         fps = n / (ms / 1e3)
         rec = {"p": p, "fps": fps, "ms": ms, "reuse_all": st["reuse_all"], "reuse_nonI": st["reuse_nonI"],
+               "wave_ring": st["wave_ring"], "fps_serial_waves": n / (ms_ser / 1e3),
                "flops_exec_per_frame": st["flops_exec"] / n, "flops_dense_per_frame": dense_flops_frame(),
                "speedup_vs_own_dense": fps / dense_fps, "speedup_vs_torch_dense": fps / torch_fps}
         if a.parity_frames > 0:
@@ -119,6 +121,7 @@ def main():
         doc["sweep"].append(rec)
         print(f"p={p:<5} reuse_all={rec['reuse_all']:.3f} nonI={rec['reuse_nonI']:.3f} fps={fps:8.0f} "
               f"x{rec['speedup_vs_own_dense']:.2f} vs own dense  GFLOP/frame {rec['flops_exec_per_frame'] / 1e9:6.1f}"
+              + f"  (serial waves {rec['fps_serial_waves']:.0f}, ring {rec['wave_ring']})"
               + (f"  err {rec['parity']['max_rel_err']:.1e} cos {rec['parity']['min_cos']:.6f}" if "parity" in rec else ""))
 
     # ---- ablation ladder on n_ab = 20 k + 1 frames (k refresh groups, each with its right-edge
@@ -130,6 +133,7 @@ def main():
     o_ab = outs(n_ab)
     ms_dense_ab, _ = timed(lambda: m.embed(x, c, dense=True, out=o_ab))
     ms_full, (_, _, _, st) = timed(lambda: m.embed(x, c, out=o_ab))
+    ms_full_ser, _ = timed(lambda: m.embed(x, c, out=o_ab, serial_waves=True))
     ms_masked, _ = timed(lambda: m.embed(x, c, no_compaction=True, out=o_ab))
     ms_frame, _ = timed(lambda: m.embed(x, c, per_frame_waves=True, out=o_ab))
     xb, cb, o_g = torch.empty_like(x[:21]), torch.empty_like(c[:21]), outs(21)
@@ -146,7 +150,9 @@ def main():
     n = n_ab
     ladder = [("dense ViT (RV_DENSE)", ms_dense), ("masked dense: hard gating, no compaction (RV_NO_COMPACTION)", ms_masked),
               ("per-frame compaction (RV_WAVE_FRAME)", ms_frame),
-              ("level-batched, one refresh group resident", ms_group), ("all groups resident (default)", ms_full)]
+              ("level-batched, one refresh group resident", ms_group),
+              ("all groups resident, serial level waves (RV_SERIAL_WAVES)", ms_full_ser),
+              ("all groups resident, wavefront over layers (default)", ms_full)]
     doc["ablation"] = {"p": p, "frames": n_ab, "reuse_all": st["reuse_all"], "halo_frames_step3": halo,
                        "steps": [{"step": k, "name": nm, "ms": v, "fps": n / (v / 1e3), "speedup": ms_dense / v}
                                  for k, (nm, v) in enumerate(ladder)],

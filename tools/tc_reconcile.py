@@ -53,8 +53,10 @@ def main():
           "by ncu (×1 = FLOPs if the counter counts FLOPs, see the ratio column); rates over the ncu "
           "duration; `pipe%` = sm__pipe_tensor_cycles_active, `hmma%` = the hmma subpipe, `smem-tc%` = "
           "sm__mem_tensor_cycles_active (tensor-core operand reads).\n")
-    print("| # | GEMM | M | N | K | us | alg TF/s | utc/alg | utc TF/s | pipe% | hmma% | smem-tc% | DRAM GB/s |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+    print("`pred%` = utc TF/s / (8,192 dense bf16 FLOP per clock per SM x 148 SMs x the launch's SM clock "
+          "`sm__cycles_elapsed.avg.per_second`): the tensor-pipe activity the counted FLOPs imply.\n")
+    print("| # | GEMM | M | N | K | us | MHz | alg TF/s | utc/alg | utc TF/s | pipe% | pred% | smem-tc% | DRAM GB/s |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     agg = defaultdict(lambda: [0.0, 0.0, 0.0])
     for i, ((name, m), s) in enumerate(zip(g, seq)):
         kind, M, Nn, K = s[:4]
@@ -65,9 +67,11 @@ def main():
         agg[kind][0] += us
         agg[kind][1] += alg
         agg[kind][2] += utc
-        print(f"| {i} | {kind} | {M} | {Nn} | {K} | {us:.1f} | {alg / us / 1e6:.0f} | {utc / alg if alg else 0:.3f} | "
-              f"{utc / us / 1e6:.0f} | {m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
-              f"{m.get('sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | "
+        clk = m.get("sm__cycles_elapsed.avg.per_second", 0.0)
+        pred = utc / (us * 1e-6) / (8192.0 * 148 * clk) * 100 if clk else 0.0
+        print(f"| {i} | {kind} | {M} | {Nn} | {K} | {us:.1f} | {clk / 1e6:.0f} | {alg / us / 1e6:.0f} | "
+              f"{utc / alg if alg else 0:.3f} | {utc / us / 1e6:.0f} | "
+              f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | {pred:.1f} | "
               f"{m.get('sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | {dram / us / 1e3:.0f} |")
     print("\n| GEMM class (layer 0) | us | alg TF/s | utc/alg | utc TF/s | frac of sustained bf16 peak (utc) |")
     print("|---|---|---|---|---|---|")
@@ -76,15 +80,18 @@ def main():
         print(f"| {k} | {us:.0f} | {alg / us / 1e6:.0f} | {utc / alg if alg else 0:.3f} | {utc / us / 1e6:.0f} | "
               f"{utc / us / 1e6 / pk:.2f} |" if pk else f"| {k} | {us:.0f} | {alg / us / 1e6:.0f} | | | |")
     a = load(os.path.join(d, "tc_attn.csv"))
-    print("\n| attention wave | frames | queries | us | alg TF/s (4 nq T D) | utc/alg | utc TF/s | pipe% | DRAM GB/s |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("\n| attention wave | frames | queries | us | alg TF/s (4 nq T D) | utc/alg | utc TF/s | pipe% | pred% | DRAM GB/s |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for w, (name, m) in enumerate(a):
         us = m["gpu__time_duration.sum"] / 1e3
         alg = 4.0 * MC[w] * T * D
         utc = m.get("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32.sum", 0.0)
         dram = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+        clk = m.get("sm__cycles_elapsed.avg.per_second", 0.0)
+        pred = utc / (us * 1e-6) / (8192.0 * 148 * clk) * 100 if clk else 0.0
         print(f"| {w} | {frames[w]} | {MC[w]} | {us:.1f} | {alg / us / 1e6:.0f} | {utc / alg:.3f} | {utc / us / 1e6:.0f} | "
-              f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | {dram / us / 1e3:.0f} |")
+              f"{m.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):.1f} | {pred:.1f} | "
+              f"{dram / us / 1e3:.0f} |")
 
 
 if __name__ == "__main__":
