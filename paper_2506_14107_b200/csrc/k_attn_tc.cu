@@ -160,7 +160,7 @@ RV_DEV uint32_t idesc64(int N, int b_mn, int M = A8_QROWS) {
          ((uint32_t)(M >> 4) << 24);
 }
 // MN-major operand spanning two 64-wide N blocks `lbo` bytes apart (leading byte offset)
-RV_DEV uint64_t sdesc_lbo(uint32_t addr, uint32_t lbo) {
+[[maybe_unused]] RV_DEV uint64_t sdesc_lbo(uint32_t addr, uint32_t lbo) {
   return sdesc(addr) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
 }
 // 16x32bx2 shapes: lanes 0-15 access TMEM lanes base..base+15 at columns [c, c+n), lanes 16-31
@@ -510,6 +510,8 @@ __global__ void __launch_bounds__(A8_THREADS, 1)
       int js = 0, jp = 0, j_end = 0x7fffffff;
       while (jp < j_end) {
         const int js0 = js, jp0 = jp;
+        (void)js0;
+        (void)jp0;
         if (js < j_end) {
           const int qs = js % A8_NQ;
           if (mbar_test(&q_full[qs], (js / A8_NQ) & 1)) {

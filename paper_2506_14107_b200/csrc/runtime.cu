@@ -63,7 +63,10 @@ thread_local std::string g_create_err;
 
 // Level waves of at most this many frames may use the wavefront schedule; larger waves fill the
 // GPU on their own (the 7,200-frame workload's 360-1,440-frame waves run serially).
-constexpr int kWavefrontMaxWave = 512;
+#ifndef RV_WF_MAX_WAVE   // experiment builds (build_variant) may raise it
+#define RV_WF_MAX_WAVE 512
+#endif
+constexpr int kWavefrontMaxWave = RV_WF_MAX_WAVE;
 
 }  // namespace
 

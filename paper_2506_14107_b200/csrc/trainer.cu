@@ -918,6 +918,7 @@ cudaError_t backward(rv_trainer* tr, int B, float tau, cudaStream_t s) {
                 *a1 = tr->a1 + o1 * Fh, *g1 = tr->g1 + o1 * Fh, *Ct = tr->Ct + oD, *dl = tr->dl + oD,
                 *r1 = tr->r1 + o1 * Hr, *r1a = tr->r1a + o1 * Hr, *Rh = tr->Rh + oD, *M = tr->M + o1;
     (void)h1;
+    (void)g1;
     const int* prov = tr->prov + o1;
     const float* Pa = tr->Pa + (size_t)l * tr->F * H * T * T;
     float* gP = tr->dP;
