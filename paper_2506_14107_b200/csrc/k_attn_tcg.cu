@@ -270,11 +270,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           const GTile& x = e ? B : A;
           const long long fb = (long long)x.slot * T + (long long)x.t * G_ROWS;
           const bf16* src = qbuf + q_col + x.h * 64 + cc * 8;
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            const int r = (lane >> 3) + 4 * i;
-            const long long row = __ldg(kvsrc + fb + min(r, x.nr - 1));
-            cp_async16(pslot + e * G_QTILE + (uint32_t)r * 128 + ((cc ^ (r & 7)) << 4), src + row * q_ld);
+#pragma unroll 1
+          for (int i0 = 0; i0 < 32; i0 += 16) {
+            int qrow[16];   // 16 table reads in flight before the copies (two latencies per tile, not 8)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) qrow[i] = __ldg(kvsrc + fb + min((lane >> 3) + 4 * (i0 + i), x.nr - 1));
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int r = (lane >> 3) + 4 * (i0 + i);
+              cp_async16(pslot + e * G_QTILE + (uint32_t)r * 128 + ((cc ^ (r & 7)) << 4), src + (long long)qrow[i] * q_ld);
+            }
           }
         }
       }
