@@ -544,6 +544,9 @@ def main():
             "waves": waves_info,
             "flops_exec_per_step": stats["flops_exec"], "flops_dense_per_step": stats["flops_dense"],
             "tc_frac_exec": stats["flops_exec"] / (ms / 1e3) / 1e12 / peaks["tc_sustained"],
+            # whole-step HBM fraction on the algorithmic bytes model (60 D B per
+            # recomputed token-layer, 18 D B per reused one)
+            "hbm_frac_alg": stats["bytes_alg"] / (ms / 1e3) / 1e9 / peaks["hbm"],
             "gemm": {"ms_per_step": gemm_ms, "tflops": gemm_fl / max(gemm_ms, 1e-9) / 1e9,
                      "frac": gemm_fl / max(gemm_ms, 1e-9) / 1e9 / peaks["tc_sustained"]},
             "roofline": roof, "kernels": kernels, "profiled_ms_sum": step_ms_prof,

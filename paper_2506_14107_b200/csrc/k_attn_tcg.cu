@@ -38,6 +38,10 @@
 namespace rv {
 namespace {
 
+// pairs of scores out of every 8 whose 2^x runs on the FMA pipe (ex2_poly2) instead of MUFU
+#ifndef AG_POLY
+#define AG_POLY 0
+#endif
 constexpr int G_THREADS = 12 * 32;
 constexpr int G_ROWS = 128;                             // query rows per tile = MMA M
 constexpr int G_KC = 96;                                // keys per chunk = S MMA N
@@ -498,9 +502,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
           for (int i = 0; i < G_KC; i += 2) {
-            const float2 x = f2unpack(ffma2(f2pack(v[i], v[i + 1]), sc2, nm2));
-            v[i] = ex2f_fast(x.x);
-            v[i + 1] = ex2f_fast(x.y);
+            const unsigned long long x2 = ffma2(f2pack(v[i], v[i + 1]), sc2, nm2);
+            if (((i >> 1) & 7) < AG_POLY) {   // this pair on the FMA pipe (MUFU relief)
+              const float2 e = f2unpack(ex2_poly2(x2));
+              v[i] = e.x;
+              v[i + 1] = e.y;
+            } else {
+              const float2 x = f2unpack(x2);
+              v[i] = ex2f_fast(x.x);
+              v[i + 1] = ex2f_fast(x.y);
+            }
             acc[(i >> 1) & 3] = fadd2(acc[(i >> 1) & 3], f2pack(v[i], v[i + 1]));
           }
           const float2 s01 = f2unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));

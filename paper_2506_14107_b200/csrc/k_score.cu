@@ -19,12 +19,12 @@ namespace rv {
 namespace {
 
 constexpr int SCORE_THREADS = 256;
-// tokens per CTA (8 warps x 8 tokens): grid = n_w x ceil(N / 64).  Bench at 7,200 frames (score
-// ms per step, 3 CTAs per SM): 16 -> 83.8, 32 -> 79.1, 64 -> 77.1-77.4, 128 -> 79.3, 256 -> 84.7
-#ifndef RV_SCORE_TOK
-#define RV_SCORE_TOK 64
-#endif
-constexpr int SCORE_TOK = RV_SCORE_TOK;
+// tokens per CTA: grid = n_w x ceil(N / tok).  Large waves take 64 (8 warps x 8 tokens; bench at
+// 7,200 frames, score ms per step, 3 CTAs per SM: 16 -> 83.8, 32 -> 79.1, 64 -> 77.1-77.4,
+// 128 -> 79.3, 256 -> 84.7); small waves (a few frames: short clips, the wavefront schedule)
+// take fewer tokens per CTA until the grid fills the GPU, so a warp's tokens are not a serial
+// latency chain.  Per-token work is independent of the split: results do not change.
+constexpr int SCORE_TOK = 64;
 
 // VPL > 0: D == 128 * VPL, the token's 3 x VPL float4 per lane are loaded unconditionally
 // (a missing reference re-reads the current row, an L1 hit) and without a loop-carried branch,
@@ -42,11 +42,11 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
                  const float* __restrict__ codec, const uint8_t* force,
                  const float* __restrict__ gate, int Hg, int dense, uint8_t* masks, float* scores,
                  uint8_t* __restrict__ wmask, uint8_t* __restrict__ wprov, int* __restrict__ cntR,
-                 bf16* __restrict__ dfull) {
+                 bf16* __restrict__ dfull, int tok) {
   __shared__ int s_reused;
   const int w = blockIdx.x;
-  const int i_beg = 1 + blockIdx.y * SCORE_TOK;
-  const int i_end = min(N, i_beg + SCORE_TOK - 1);
+  const int i_beg = 1 + blockIdx.y * tok;
+  const int i_end = min(N, i_beg + tok - 1);
   const int4 d4 = wdesc[w];
   const int slot = d4.x, past = d4.y, fut = d4.z, type = d4.w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,11 +270,13 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
   if (n_w <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(cntR, 0, (size_t)n_w * sizeof(int), s);
   if (e != cudaSuccess) return e;
-  dim3 grid(n_w, (N + SCORE_TOK - 1) / SCORE_TOK);
+  int tok = SCORE_TOK;
+  while (tok > SCORE_THREADS / 32 && (long long)n_w * ((N + tok - 1) / tok) < 3LL * dev_sms()) tok >>= 1;
+  dim3 grid(n_w, (N + tok - 1) / tok);
   const int4* wd = reinterpret_cast<const int4*>(wdesc);
 #define RV_SCORE(V)                                                                                              \
   score_kernel<V><<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, wd, tsrc, tH, codec, force, gate, Hg, dense, \
-                                                 masks, scores, wmask, wprov, cntR, dfull)
+                                                 masks, scores, wmask, wprov, cntR, dfull, tok)
   if (D == 1024) RV_SCORE(8);
   else if (D == 768) RV_SCORE(6);
   else RV_SCORE(0);

@@ -147,4 +147,27 @@ RV_DEV unsigned long long fadd2(unsigned long long a, unsigned long long b) {
   return d;
 }
 
+// 2^x for a pair on the FMA / ALU pipes (no MUFU): round-to-nearest through the 1.5 * 2^23
+// magic number, 2^f on f in [-0.5, 0.5] by a degree-4 polynomial (max relative error 2.7e-6,
+// below the bf16 rounding of P), then the integer part added to the exponent field.  x is
+// clamped to -125, so masked (-inf) scores give 2^-125 instead of 0 (negligible against a row
+// whose maximum term is 1).
+RV_DEV unsigned long long ex2_poly2(unsigned long long x2) {
+  float2 x = f2unpack(x2);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const unsigned long long magic = f2pack(12582912.f, 12582912.f), nmagic = f2pack(-12582912.f, -12582912.f);
+  const unsigned long long t = fadd2(f2pack(x.x, x.y), magic);
+  const float2 r = f2unpack(fadd2(t, nmagic));
+  const unsigned long long f = f2pack(x.x - r.x, x.y - r.y);
+  unsigned long long p = f2pack(0.00957007147371769f, 0.00957007147371769f);
+  p = ffma2(p, f, f2pack(0.05591777339577675f, 0.05591777339577675f));
+  p = ffma2(p, f, f2pack(0.240247443318367f, 0.240247443318367f));
+  p = ffma2(p, f, f2pack(0.6931218504905701f, 0.6931218504905701f));
+  p = ffma2(p, f, f2pack(0.9999992847442627f, 0.9999992847442627f));
+  const float2 tv = f2unpack(t), pv = f2unpack(p);
+  return f2pack(__uint_as_float(__float_as_uint(pv.x) + (__float_as_uint(tv.x) << 23)),
+                __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23)));
+}
+
 }  // namespace rv
