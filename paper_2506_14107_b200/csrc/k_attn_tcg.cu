@@ -42,7 +42,14 @@ namespace {
 #ifndef AG_POLY
 #define AG_POLY 0
 #endif
-constexpr int G_THREADS = 12 * 32;
+// 16 warps: loaders 0-1, issuer of group 0 (2), producer (3), softmax groups 4-7 and 8-11,
+// issuer of group 1 (12), 13-15 idle.  Registers: warpgroups 0 and 3 drop to G_REG_LO, the two
+// softmax warpgroups take G_REG_HI (2 x 128 x 80 + 256 x 176 = 65,536).
+constexpr int G_THREADS = 16 * 32;
+#define G_REG_LO 80
+#define G_REG_HI 176
+#define G_STR2(x) #x
+#define G_STR(x) G_STR2(x)
 constexpr int G_ROWS = 128;                             // query rows per tile = MMA M
 constexpr int G_KC = 96;                                // keys per chunk = S MMA N
 constexpr int G_MAXNC = 11;                             // chunks: T - 1 <= 1056
@@ -78,8 +85,8 @@ struct GTile {
 #ifdef RV_AG_TRACE   // experiment builds: event timeline of CTA 0 (printed at exit)
 // each tracing thread appends to its own region (no atomics: the trace must not perturb timing)
 constexpr int AG_REG = 2048;
-__device__ unsigned long long g_ag_trace[6 * AG_REG][2];
-__device__ int g_ag_cnt[6];
+__device__ unsigned long long g_ag_trace[7 * AG_REG][2];
+__device__ int g_ag_cnt[7];
 RV_DEV void ag_tr(int region, int& n, int code) {
   if (blockIdx.x != 0 || n >= AG_REG) return;
   unsigned long long t;
@@ -120,11 +127,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
     for (int i = 0; i < G_NK; ++i) {
       mbar_init(&kf[i], 64);
-      mbar_init(&ke[i], 1);
+      mbar_init(&ke[i], 2);   // two commits per use (one per issuer, or both from the only reader)
     }
     for (int i = 0; i < G_NV; ++i) {
       mbar_init(&vf[i], 64);
-      mbar_init(&ve[i], 1);
+      mbar_init(&ve[i], 2);
     }
     for (int i = 0; i < G_NI; ++i) {
       mbar_init(&i_full[i], 1);
@@ -150,10 +157,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 
 #ifdef RV_AG_TRACE
   int ag_n = 0;
-  const int ag_region = warp < 4 ? (warp == 3 ? 2 : (warp == 2 ? 3 : warp)) : (warp == 4 ? 4 : 5);
+  const int ag_region = warp < 4 ? (warp == 3 ? 2 : (warp == 2 ? 3 : warp)) : (warp == 12 ? 6 : (warp == 4 ? 4 : 5));
 #endif
   if (warp < 2) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " G_STR(G_REG_LO) ";" ::: "memory");
     // ======================================================================== K / V loaders
     // Consume the producer's chunk tables in sequence order: 16 row indices per lane from shared
     // memory, then the K rows, then the V rows of the chunk (cp.async, 8 lanes per 128 B row).
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       if (lane == 0) AG_TR(1, 3, seq, warp);
     }
   } else if (warp == 3) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " G_STR(G_REG_LO) ";" ::: "memory");
     // ======================================================================== producer
     // Walks the CTA's frame-head stream (fh = blockIdx.x + k gridDim.x, head fastest), forms
     // pairs of tiles, publishes each pair's descriptor and Q / CLS loads, and writes the row
@@ -314,32 +321,40 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
       cp_async_arrive(&q_full[ps]);
     }
-  } else if (warp == 2) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
-    // ======================================================================== MMA issuer
-    // Pairs in order, both tiles in lockstep: S(x, 0); then per chunk c: S(x, c + 1) into the
-    // other S buffer (so the softmax of chunk c + 1 can start as soon as chunk c is done), then
-    // O_x (+)= P(x, c) V(c) once group x stored P.  MMAs of this thread execute in issue order,
-    // so S(c + 2) overwrites P(c) only after P V(c) has read it.
-    if (lane == 0) {
+  } else if (warp == 2 || warp >= 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " G_STR(G_REG_LO) ";" ::: "memory");
+    // ======================================================================== MMA issuers
+    // One issuing thread per softmax group (warp 2: group 0, warp 12: group 1): a thread issues
+    // at most one tcgen05.mma every ~120 cycles whatever its size, and the attention's MMAs are
+    // small (N = 96 / 64), so two issuers double the MMA rate (tools/umma_issuers.cu: 120 -> 60
+    // cycles per M = 128, N = 64 MMA).  Per pair, group g: S(g, 0); per chunk c: S(g, c + 1) into
+    // the other S buffer (its softmax starts chunk c + 1 as soon as chunk c is done), then
+    // O_g (+)= P(g, c) V(c) once the group stored P.  MMAs of one thread execute in issue order,
+    // so S(c + 2) overwrites P(c) only after P V(c) has read it.  K / V ring slots: their empty
+    // barriers count 2 arrivals; each issuer commits once per slot it read, a slot read by one
+    // group only (separate tiles, or a pair without a second tile) gets both commits from it.
+    const int g = warp == 2 ? 0 : 1;
+    if (lane == 0 && warp <= 12) {
       const uint32_t id_o = idesc_f16(G_ROWS, 64, 1);
-      uint32_t kpend = 0, vpend = 0;   // shared ring slots whose first consumer has issued
-      int nch[2] = {0, 0}, ntl[2] = {0, 0}, ns[2] = {0, 0};
+      int nch = 0, ntl = 0, ns = 0;
       for (int p = 0;; ++p) {
         const int ps = p % G_NQ;
         mbar_wait(&q_full[ps], (uint32_t)(p / G_NQ) & 1);
         const volatile GMeta& m = meta[ps];
         if (m.done) break;
-        const int ng = m.has_b ? 2 : 1, seq0 = m.seq0, stride = m.stride;
+        if (g == 1 && !m.has_b) continue;
+        const int seq0 = m.seq0, stride = m.stride;
         const bool shared = m.shared;
-        auto issue_s = [&](int g, int c) {
-          const int seq = seq0 + c * stride + ((g == 1 && !shared) ? 1 : 0);
+        const int nrel = (shared && m.has_b) ? 1 : 2;   // commits this group owes each slot it reads
+        const int seq_g = seq0 + ((g == 1 && !shared) ? 1 : 0);
+        auto issue_s = [&](int c) {
+          const int seq = seq_g + c * stride;
           const uint32_t ks = (uint32_t)seq % G_NK;
           mbar_wait(&kf[ks], (uint32_t)(seq / G_NK) & 1);
-          // every mbarrier here may run at most one phase ahead of its waiter: S number k of a
+          // every mbarrier here may run at most one phase ahead of its waiter: S number k of the
           // group is issued only once its softmax has taken S number k - 1
-          if (ns[g] > 0) mbar_wait(&s_taken[g], (uint32_t)(ns[g] - 1) & 1);
-          ++ns[g];
+          if (ns > 0) mbar_wait(&s_taken[g], (uint32_t)(ns - 1) & 1);
+          ++ns;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor core
           tc_after();
           const int nS = (min(G_KC, NP - c * G_KC) + 15) & ~15;
@@ -349,20 +364,15 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) mma_ss(tS, sdesc(qa + k * 32), sdesc(ka + k * 32), id_s, k != 0);
           mma_commit(&s_full[g]);
-          if (shared && !((kpend >> ks) & 1)) {
-            kpend |= 1u << ks;
-          } else {
-            kpend &= ~(1u << ks);
-            mma_commit(&ke[ks]);
-          }
+          for (int r = 0; r < nrel; ++r) mma_commit(&ke[ks]);
           AG_TR(2, 0, seq, g);
         };
-        auto issue_pv = [&](int g, int c) {
-          const int seq = seq0 + c * stride + ((g == 1 && !shared) ? 1 : 0);
+        auto issue_pv = [&](int c) {
+          const int seq = seq_g + c * stride;
           const uint32_t vs = (uint32_t)seq % G_NV;
-          mbar_wait(&p_full[g], (uint32_t)nch[g] & 1);
+          mbar_wait(&p_full[g], (uint32_t)nch & 1);
           mbar_wait(&vf[vs], (uint32_t)(seq / G_NV) & 1);
-          if (c == 0) mbar_wait(&r_free[g], ((uint32_t)ntl[g] & 1) ^ 1);   // previous tile's O read
+          if (c == 0) mbar_wait(&r_free[g], ((uint32_t)ntl & 1) ^ 1);   // previous tile's O read
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_after();
           const int nS = (min(G_KC, NP - c * G_KC) + 15) & ~15;
@@ -371,26 +381,20 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           for (int k = 0; k < nS / 16; ++k)   // O (+)= P V: 16 keys per MMA, P packed at column 8 k
             mma_ts(tO, tS + (uint32_t)(k * 8), sdesc(va + (uint32_t)k * 2048), id_o, (c | k) != 0);
           mma_commit(&pv_full[g]);
-          if (shared && !((vpend >> vs) & 1)) {
-            vpend |= 1u << vs;
-          } else {
-            vpend &= ~(1u << vs);
-            mma_commit(&ve[vs]);
-          }
-          ++nch[g];
+          for (int r = 0; r < nrel; ++r) mma_commit(&ve[vs]);
+          ++nch;
           AG_TR(2, 1, seq, g);
         };
-        for (int g = 0; g < ng; ++g) issue_s(g, 0);
+        issue_s(0);
         for (int c = 0; c < nc; ++c) {
-          if (c + 1 < nc)
-            for (int g = 0; g < ng; ++g) issue_s(g, c + 1);
-          for (int g = 0; g < ng; ++g) issue_pv(g, c);
+          if (c + 1 < nc) issue_s(c + 1);
+          issue_pv(c);
         }
-        for (int g = 0; g < ng; ++g) ++ntl[g];
+        ++ntl;
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 " G_STR(G_REG_HI) ";" ::: "memory");
     // ======================================================================== softmax groups
     const int g = (warp - 4) >> 2;
     const int q = warp & 3;                            // TMEM lane quarter
@@ -585,7 +589,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   __syncthreads();
 #ifdef RV_AG_TRACE
   if (blockIdx.x == 0 && tid == 0) {
-    for (int r = 0; r < 6; ++r) {
+    for (int r = 0; r < 7; ++r) {
       for (int i = 0; i < g_ag_cnt[r]; ++i)
         printf("AG %llx %llu\n", g_ag_trace[r * AG_REG + i][0], g_ag_trace[r * AG_REG + i][1]);
       g_ag_cnt[r] = 0;
