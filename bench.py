@@ -321,10 +321,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tests/test_gpu_bench_multirank.py): every rank on cuda:0 over gloo, so the N > 1
+    # code path (sharding, halo, gather, max over ranks, rank-0 line) runs on a one-GPU box
+    one_gpu = os.environ.get("RV_BENCH_GLOO_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     wl = setup_c5(args, world, rank, dev) if args.workload == "c5" else setup_video(args, world, rank, dev)
     cfg, x, c, plan = wl["cfg"], wl["x"], wl["c"], wl["plan"]
     L, N, T, D = cfg.layers, cfg.N, cfg.T, cfg.dim

@@ -386,13 +386,18 @@ def test_keep_all_cache_ablation(cuda_ok):
     m, W, G = build(cfg)
     x, c = synth.make_video(cfg, 41, 0.2, seed=45)
     xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c).cuda()
-    Z1, M1, _, s1 = m.embed(xd, cd)
+    Z1, M1, _, s1 = m.embed(xd, cd, serial_waves=True)
     Z2, M2, _, s2 = m.embed(xd, cd, keep_all_cache=True)
+    Z3, M3, _, s3 = m.embed(xd, cd)      # default: wavefront over a ring of R layer buffers
     torch.cuda.synchronize()
-    assert torch.equal(M1, M2) and torch.equal(Z1, Z2)
+    assert torch.equal(M1, M2) and torch.equal(Z1, Z2) and torch.equal(M1, M3) and torch.equal(Z1, Z3)
     L, T, D, n = cfg.layers, cfg.T, cfg.dim, 41
     assert s1["peak_cache_bytes"] == n * T * D * (2 * 4 + 2 * 2)
     assert s2["peak_cache_bytes"] == n * T * D * ((L + 1) * 4 + L * 2 * 2)
+    R = s3["wave_ring"]   # R X slots (fp32), R - 1 K/V slots (bf16 K|V) and R - 1 source-row tables
+    assert 3 <= R <= L + 1
+    assert s3["peak_cache_bytes"] == n * T * D * (2 * 4 + 2 * 2) + (R - 2) * (n * T * D * (4 + 2 * 2) + n * T * 4)
+    assert s3["peak_cache_bytes"] < s2["peak_cache_bytes"]
     assert s2["device_bytes"] > s1["device_bytes"]
     # the bench workload: 7,200 frames of ViT-L/14
     cfg = synth.CONFIGS["l14"]
