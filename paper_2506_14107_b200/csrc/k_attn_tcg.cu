@@ -42,8 +42,8 @@ namespace {
 #ifndef AG_POLY
 #define AG_POLY 0
 #endif
-// 16 warps: loaders 0-1, issuer of group 0 (2), producer (3), softmax groups 4-7 and 8-11,
-// issuer of group 1 (12), 13-15 idle.  Registers: warpgroups 0 and 3 drop to G_REG_LO, the two
+// 16 warps: K loaders 0 and 13, V loaders 1 and 14, issuer of group 0 (2), producer (3),
+// softmax groups 4-7 and 8-11, issuer of group 1 (12), 15 idle.  Registers: warpgroups 0 and 3 drop to G_REG_LO, the two
 // softmax warpgroups take G_REG_HI (2 x 128 x 80 + 256 x 176 = 65,536).
 constexpr int G_THREADS = 16 * 32;
 #define G_REG_LO 80
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
     for (int i = 0; i < G_NI; ++i) {
       mbar_init(&i_full[i], 1);
-      mbar_init(&i_empty[i], 2);   // both loader warps
+      mbar_init(&i_empty[i], 4);   // the four loader warps
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
@@ -159,13 +159,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   int ag_n = 0;
   const int ag_region = warp < 4 ? (warp == 3 ? 2 : (warp == 2 ? 3 : warp)) : (warp == 12 ? 6 : (warp == 4 ? 4 : 5));
 #endif
-  if (warp < 2) {
+  if (warp < 2 || warp == 13 || warp == 14) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 " G_STR(G_REG_LO) ";" ::: "memory");
     // ======================================================================== K / V loaders
-    // Consume the producer's chunk tables in sequence order: 16 row indices per lane from shared
-    // memory, then the K rows, then the V rows of the chunk (cp.async, 8 lanes per 128 B row).
+    // Consume the producer's chunk tables in sequence order.  Warps 0 and 13 load the K rows,
+    // warps 1 and 14 the V rows (each warp half of the 96 rows, cp.async, 8 lanes per 128 B
+    // row): a K load never queues behind a V slot, which frees only after P V, late in the
+    // chunk's chain (ncu: with one loader stream per warp the loaders waited on V slots while
+    // the softmax waited on S).
+    const bool is_v = warp == 1 || warp == 14;
+    const int part = warp < 2 ? 0 : 1;
     const int cc = lane & 7;                            // 16 B chunk of a 128 B row
-    const int rsub = warp * 4 + (lane >> 3);            // rows rsub + 8 i, i < 12
+    const int rsub = part * 4 + (lane >> 3);            // rows rsub + 8 i, i < 12
+    const uint32_t nslot = is_v ? G_NV : G_NK;
+    uint64_t* full = is_v ? vf : kf;
+    uint64_t* empty = is_v ? ve : ke;
+    const uint32_t ring = base + (is_v ? G_VR : G_KR);
     for (int seq = 0;; ++seq) {
       const int ti = seq % G_NI;
       mbar_wait(&i_full[ti], (uint32_t)(seq / G_NI) & 1);
@@ -178,24 +187,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       for (int i = 0; i < G_KC / 8; ++i) idx[i] = tab[4 + rsub + 8 * i];
       __syncwarp();
       if (lane == 0) mbar_arrive(&i_empty[ti]);
-      const uint32_t ks = (uint32_t)seq % G_NK, vs = (uint32_t)seq % G_NV;
-      const bf16* src = KV + h * 64 + cc * 8;
-      mbar_wait(&ke[ks], ((uint32_t)(seq / G_NK) & 1) ^ 1);
-      const uint32_t kd = base + G_KR + ks * G_KVTILE;
+      const uint32_t sl = (uint32_t)seq % nslot;
+      const bf16* src = KV + (is_v ? D : 0) + h * 64 + cc * 8;
+      mbar_wait(&empty[sl], ((uint32_t)(seq / nslot) & 1) ^ 1);
+      const uint32_t dst = ring + sl * G_KVTILE;
 #pragma unroll
       for (int i = 0; i < G_KC / 8; ++i) {
         const int r = rsub + 8 * i;
-        if (8 * i < nS) cp_async16(kd + (uint32_t)r * 128 + ((cc ^ (r & 7)) << 4), src + (long long)idx[i] * kv_ld);
+        if (8 * i < nS) cp_async16(dst + (uint32_t)r * 128 + ((cc ^ (r & 7)) << 4), src + (long long)idx[i] * kv_ld);
       }
-      cp_async_arrive(&kf[ks]);
-      mbar_wait(&ve[vs], ((uint32_t)(seq / G_NV) & 1) ^ 1);
-      const uint32_t vd = base + G_VR + vs * G_KVTILE;
-#pragma unroll
-      for (int i = 0; i < G_KC / 8; ++i) {
-        const int r = rsub + 8 * i;
-        if (8 * i < nS) cp_async16(vd + (uint32_t)r * 128 + ((cc ^ (r & 7)) << 4), src + D + (long long)idx[i] * kv_ld);
-      }
-      cp_async_arrive(&vf[vs]);
+      cp_async_arrive(&full[sl]);
       if (lane == 0) AG_TR(1, 3, seq, warp);
     }
   } else if (warp == 3) {
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
       cp_async_arrive(&q_full[ps]);
     }
-  } else if (warp == 2 || warp >= 12) {
+  } else if (warp == 2 || warp == 12 || warp == 15) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 " G_STR(G_REG_LO) ";" ::: "memory");
     // ======================================================================== MMA issuers
     // One issuing thread per softmax group (warp 2: group 0, warp 12: group 1): a thread issues
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     // barriers count 2 arrivals; each issuer commits once per slot it read, a slot read by one
     // group only (separate tiles, or a pair without a second tile) gets both commits from it.
     const int g = warp == 2 ? 0 : 1;
-    if (lane == 0 && warp <= 12) {
+    if (lane == 0 && warp != 15) {
       const uint32_t id_o = idesc_f16(G_ROWS, 64, 1);
       int nch = 0, ntl = 0, ns = 0;
       for (int p = 0;; ++p) {
