@@ -258,6 +258,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       const bool shared = has_b && B.fh == A.fh, sep = has_b && !shared;
       const int ps = p % G_NQ;
       const uint32_t pslot = base + (uint32_t)ps * G_PSLOT;
+      // the pair's K / V chunk tables first: the loaders start on them while this pair's Q slot
+      // is still held by the pair before last (its epilogue), instead of after the Q loads
+      const int seq_p = seq;
+      for (int c = 0; c < nc; ++c) {   // chunk loads: chunk-major, tile a then (unless shared) tile b
+        put_table(&A, c);
+        if (sep) put_table(&B, c);
+      }
       if (lane == 0) AG_TR(1, 0, p, 0);
       mbar_wait(&q_empty[ps], ((uint32_t)(p / G_NQ) & 1) ^ 1);
       if (lane == 0) AG_TR(1, 1, p, has_b * 2 + shared);
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           m.q0[e] = xs[e]->q0; m.nr[e] = xs[e]->nr; m.slot[e] = xs[e]->slot; m.h[e] = xs[e]->h; m.tile[e] = xs[e]->t;
         }
-        m.seq0 = seq; m.stride = sep ? 2 : 1; m.shared = shared; m.has_b = has_b; m.done = 0;
+        m.seq0 = seq_p; m.stride = sep ? 2 : 1; m.shared = shared; m.has_b = has_b; m.done = 0;
         if (q_mode == 0) {
           mbar_expect_tx(&q_full[ps], G_QTILE * (has_b ? 2 : 1));
           for (int e = 0; e < (has_b ? 2 : 1); ++e)
@@ -305,10 +312,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         }
       }
       cp_async_arrive(&q_full[ps]);
-      for (int c = 0; c < nc; ++c) {   // chunk loads: chunk-major, tile a then (unless shared) tile b
-        put_table(&A, c);
-        if (sep) put_table(&B, c);
-      }
       ++p;
     }
     // end markers: the loaders' table stream and the next pair slot

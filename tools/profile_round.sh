@@ -19,4 +19,6 @@ timeout 600 $NCU -k regex:attn_tc --launch-skip 3 -o $O/prof_${R}_attn python to
 timeout 600 $NCU -k regex:score_kernel --launch-skip 3 -o $O/prof_${R}_score python tools/prof_run.py --frames 1440 > /dev/null 2>&1
 timeout 600 $NCU -k regex:gemm_tc_kernel --launch-skip 19 -o $O/prof_${R}_fc1 python tools/prof_run.py --frames 1440 > /dev/null 2>&1
 timeout 600 $NCU -k regex:gemm_tc_kernel --launch-skip 22 -o $O/prof_${R}_r2 python tools/prof_run.py --frames 1440 > /dev/null 2>&1
+# the general tcgen05 attention (L/14@336, T = 577; BASELINE configs[4] shape), level-3 wave
+timeout 600 $NCU -k regex:attn_tcg --launch-skip 3 -o $O/prof_${R}_attng python tools/prof_run.py --config l14_336 --frames 480 > /dev/null 2>&1
 ls -la $O | tail -20
