@@ -63,7 +63,9 @@ rv_status rv_stage_gemm_rows(rv_ctx* ctx, int32_t M, int32_t N, int32_t K, const
 
 /* a8 — attention of compacted queries over all T keys of their frame:
  * q [M_C][D] bf16 (rows qoff[w]..qoff[w+1]-1 belong to wave frame w, first row = CLS),
- * KV [slots][T][2D] bf16 (K in columns 0..D-1, V in D..2D-1, head h = columns h*dh..),
+ * KV [slots][T][2D] bf16, per token row head-interleaved: head h's key in columns
+ *    2h*dh..2h*dh+dh-1 and its value in the next dh columns (the layout the embed's QKV GEMM
+ *    writes: one 2*dh segment per (token, head), 256 B at d_h = 64),
  * out [M_C][D] bf16 = softmax(q K^T / sqrt(dh)) V per head; pcls [slots][H][N] fp32 (or
  * NULL) = per-head CLS softmax row over the patch keys; its head mean is t for the next
  * layer.  q_rows = allocated rows of q (>= qoff[n_w]; the tcgen05 path

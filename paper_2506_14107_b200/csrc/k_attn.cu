@@ -47,9 +47,9 @@ RV_DEV void load_kv_block(bf16* Kb, bf16* Vb, const bf16* __restrict__ KV, const
   for (int idx = tid; idx < nrow * CH; idx += 128) {
     const int j = idx / CH, c = idx % CH;
     const bool ok = k0 + j < T;
-    const bf16* kr = KV + (long long)rows_s[k0 + j] * ld + h * DH + c * 8;
+    const bf16* kr = KV + (long long)rows_s[k0 + j] * ld + h * 2 * DH + c * 8;   // (k_h v_h) per token
     cp_async16(Kb + j * KS + c * 8, kr, ok);
-    cp_async16(Vb + j * KS + c * 8, kr + D, ok);
+    cp_async16(Vb + j * KS + c * 8, kr + DH, ok);
   }
 }
 

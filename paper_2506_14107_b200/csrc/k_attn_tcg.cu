@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&i_empty[ti]);
       const uint32_t sl = (uint32_t)seq % nslot;
-      const bf16* src = KV + (is_v ? D : 0) + h * 64 + cc * 8;
+      const bf16* src = KV + h * 128 + (is_v ? 64 : 0) + cc * 8;   // (k_h v_h) per token
       mbar_wait(&empty[sl], ((uint32_t)(seq / nslot) & 1) ^ 1);
       const uint32_t dst = ring + sl * G_KVTILE;
 #pragma unroll
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           const GTile& x = e ? B : A;
           const long long fb = (long long)x.slot * T;
           const long long row = kvsrc ? __ldg(kvsrc + fb) : fb;
-          cp_async16(pslot + 2 * G_QTILE + e * 256 + kv * 128 + cc * 16, KV + row * kv_ld + kv * D + x.h * 64 + cc * 8);
+          cp_async16(pslot + 2 * G_QTILE + e * 256 + kv * 128 + cc * 16, KV + row * kv_ld + x.h * 128 + kv * 64 + cc * 8);
         }
       }
       cp_async_arrive(&q_full[ps]);

@@ -1135,8 +1135,26 @@ rv_status rv_load_vit(rv_ctx* ctx, const float* blob, size_t n_floats) {
     LayerW& w = ctx->lw[l];
     if ((s = upload_f(ctx, W, &w.ln1_g, p, D))) return s; p += D;
     if ((s = upload_f(ctx, W, &w.ln1_b, p, D))) return s; p += D;
-    if ((s = upload_T(ctx, W, &w.Wqkv, p, D, 3 * D, D))) return s; p += (size_t)D * 3 * D;
-    if ((s = upload_f(ctx, W, &w.bqkv, p, 3 * D))) return s; p += 3 * D;
+    {
+      // K/V cache layout (a7): the QKV output columns q | k | v (head h = columns h*dh..) are
+      // reordered at load to q | (k_0 v_0) (k_1 v_1) ..., so one head's key and value of a token
+      // are 2*dh contiguous bf16 (256 B at d_h = 64): the attention gathers one 256 B segment per
+      // (token, head) instead of two 128 B rows 2 KB apart (tools/gather_rate.cu: 4.9 -> 6.1 TB/s)
+      std::vector<float> wq((size_t)D * 3 * D), bq(3 * D);
+      const int dh = ctx->dh;
+      auto col = [&](int j) {
+        if (j < D) return j;
+        const int kv = (j - D) / D, h = ((j - D) % D) / dh, c = (j - D) % dh;
+        return D + h * 2 * dh + kv * dh + c;
+      };
+      for (int j = 0; j < 3 * D; ++j) {
+        const int nj = col(j);
+        bq[nj] = p[(size_t)D * 3 * D + j];
+        for (int i = 0; i < D; ++i) wq[(size_t)i * 3 * D + nj] = p[(size_t)i * 3 * D + j];
+      }
+      if ((s = upload_T(ctx, W, &w.Wqkv, wq.data(), D, 3 * D, D))) return s; p += (size_t)D * 3 * D;
+      if ((s = upload_f(ctx, W, &w.bqkv, bq.data(), 3 * D))) return s; p += 3 * D;
+    }
     if ((s = upload_T(ctx, W, &w.Wo, p, D, D, D))) return s; p += (size_t)D * D;
     if ((s = upload_f(ctx, W, &w.bo, p, D))) return s; p += D;
     if ((s = upload_f(ctx, W, &w.ln2_g, p, D))) return s; p += D;

@@ -131,8 +131,8 @@ def test_attention_vs_torch(dev, cfgname, use_tc):
     torch.cuda.synchronize()
     for w in range(n_w):
         s = slot_of[w]
-        Kf = KV[s * T:(s + 1) * T, :D].float().reshape(T, H, dh).transpose(0, 1)
-        Vf = KV[s * T:(s + 1) * T, D:].float().reshape(T, H, dh).transpose(0, 1)
+        Kf = KV[s * T:(s + 1) * T].float().reshape(T, H, 2, dh)[:, :, 0].transpose(0, 1)
+        Vf = KV[s * T:(s + 1) * T].float().reshape(T, H, 2, dh)[:, :, 1].transpose(0, 1)
         qf = q[qoff[w]:qoff[w + 1]].float().reshape(-1, H, dh).transpose(0, 1)
         P = torch.softmax(qf @ Kf.transpose(1, 2) / dh ** 0.5, dim=-1)
         ref = (P @ Vf).transpose(0, 1).reshape(-1, D)
@@ -180,8 +180,8 @@ def test_attention_wave_kvsrc(dev, cfgname, use_tc):
     for w in range(n_w):
         s = int(slot_of[w])
         rows = kv_d[s].long()
-        Kf = KV[rows, :D].float().reshape(T, H, dh).transpose(0, 1)
-        Vf = KV[rows, D:].float().reshape(T, H, dh).transpose(0, 1)
+        Kf = KV[rows].float().reshape(T, H, 2, dh)[:, :, 0].transpose(0, 1)
+        Vf = KV[rows].float().reshape(T, H, 2, dh)[:, :, 1].transpose(0, 1)
         qf = q[qoff[w]:qoff[w + 1]].float().reshape(-1, H, dh).transpose(0, 1)
         P = torch.softmax(qf @ Kf.transpose(1, 2) / dh ** 0.5, dim=-1)
         ref = (P @ Vf).transpose(0, 1).reshape(-1, D)
@@ -219,8 +219,8 @@ def test_attention_tcg_online_rescale(dev, boost_block):
                       torch.cuda.current_stream(), use_tc=2)
     torch.cuda.synchronize()
     for w in range(n_w):
-        Kf = KV[w * T:(w + 1) * T, :D].float().reshape(T, H, dh).transpose(0, 1)
-        Vf = KV[w * T:(w + 1) * T, D:].float().reshape(T, H, dh).transpose(0, 1)
+        Kf = KV[w * T:(w + 1) * T].float().reshape(T, H, 2, dh)[:, :, 0].transpose(0, 1)
+        Vf = KV[w * T:(w + 1) * T].float().reshape(T, H, 2, dh)[:, :, 1].transpose(0, 1)
         qf = q[qoff[w]:qoff[w + 1]].float().reshape(-1, H, dh).transpose(0, 1)
         P = torch.softmax(qf @ Kf.transpose(1, 2) / dh ** 0.5, dim=-1)
         ref = (P @ Vf).transpose(0, 1).reshape(-1, D)

@@ -79,6 +79,11 @@ def test_compute_sanitizer(cuda_ok, tool, tmp_path):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
     log = r.stdout[-6000:] + r.stderr[-6000:]
     print(log[-3000:])
+    if "closed on this pool" in log:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (it has left GPUs needing a
+        # reset elsewhere); out-of-bounds accesses are then covered by the full-size parity and
+        # determinism tests only
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "SANITIZER_SCRIPT_OK" in r.stdout, log
     assert r.returncode == 0, log
     import re

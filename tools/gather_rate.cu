@@ -31,7 +31,7 @@ constexpr int NSLOT = 6;
 constexpr uint32_t TILE = 256 * 128;
 
 __global__ void __launch_bounds__(512, 1) gather(const __grid_constant__ CUtensorMap tm, const uint16_t* __restrict__ M,
-                                                 uint32_t R, int tiles_per_cta, int mode, int lw, unsigned long long* sink) {
+                                                 uint32_t R, int tiles_per_cta, int mode, int lw, unsigned long long* sink, int seg) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t full[NSLOT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -50,11 +50,14 @@ __global__ void __launch_bounds__(512, 1) gather(const __grid_constant__ CUtenso
       const uint32_t seed = (blockIdx.x * 100003u + t) * 256u;
       const int head = (blockIdx.x + t) & 15;
       if (mode == 0) {
-        const int c = lane & 7;
-        for (int r = warp * 4 + (lane >> 3); r < 256; r += 4 * lw) {
+        // seg B contiguous per gathered row (seg / 16 lanes per row), TILE / seg rows per tile
+        const int lpr = seg >> 4, rpw = 32 / lpr, nrow = TILE / seg;
+        const int c = lane % lpr;
+        const int hseg = head % (4096 / seg);
+        for (int r = warp * rpw + lane / lpr; r < nrow; r += rpw * lw) {
           const uint32_t row = hrow(seed + r, R);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + r * 128 + ((c ^ (r & 7)) << 4)),
-                       "l"(M + (size_t)row * 2048 + head * 64 + c * 8) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + r * seg + (((c & 7) ^ (r & 7)) << 4) + ((c >> 3) << 7)),
+                       "l"(M + (size_t)row * 2048 + hseg * (seg / 2) + c * 8) : "memory");
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
       } else {
@@ -123,12 +126,12 @@ int main() {
   const char* names[4] = {"cp.async 16B", "cp.async.bulk 128B", "TMA 2D {64,1}", "TMA gather4"};
   for (int mode = 0; mode < 4; ++mode)
     for (int lw = 1; lw <= 16; lw *= 2) {
-      gather<<<sms, 512, smem>>>(tm, d, R, 20, mode, lw, sink);
+      gather<<<sms, 512, smem>>>(tm, d, R, 20, mode, lw, sink, 128);
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a);
-      gather<<<sms, 512, smem>>>(tm, d, R, tiles, mode, lw, sink);
+      gather<<<sms, 512, smem>>>(tm, d, R, tiles, mode, lw, sink, 128);
       cudaEventRecord(b);
       cudaError_t e = cudaEventSynchronize(b);
       if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -140,6 +143,22 @@ int main() {
       const double bytes = (double)sms * tiles * TILE;
       printf("%-20s loader warps %d: %.3f ms, %.0f GB/s (%.1f GB/s per SM)\n", names[mode], lw, ms, bytes / ms / 1e6,
              bytes / ms / 1e6 / sms);
+    }
+  // segment size: K and V of one head adjacent (256 B) or two heads (512 B) per gathered row
+  for (int seg = 128; seg <= 512; seg *= 2)
+    for (int lw = 2; lw <= 8; lw *= 2) {
+      gather<<<sms, 512, smem>>>(tm, d, R, 20, 0, lw, sink, seg);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      gather<<<sms, 512, smem>>>(tm, d, R, tiles, 0, lw, sink, seg);
+      cudaEventRecord(b);
+      if (cudaEventSynchronize(b) != cudaSuccess) { printf("seg error\n"); return 1; }
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bytes = (double)sms * tiles * TILE;
+      printf("cp.async 16B seg %4d B  loader warps %d: %.3f ms, %.0f GB/s\n", seg, lw, ms, bytes / ms / 1e6);
     }
   return 0;
 }
