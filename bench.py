@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--attn-sync", action="store_true", help="mma.sync attention kernel (RV_ATTN_SYNC) instead of tcgen05")
     ap.add_argument("--chain", action="store_true", help="SPEC chain variant (RV_CHAIN, SURVEY NEXT-1) instead of D1")
+    ap.add_argument("--x-bf16", action="store_true", help="experimental bf16 residual stream (RV_X_BF16)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: the 7,200-frame L/14 video (default); c5: L/14@336 multi-video, LPT-sharded")
@@ -349,7 +350,7 @@ def main():
 
     def step(profile):
         m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync,
-                      chain=args.chain)
+                      chain=args.chain, x_bf16=args.x_bf16)
         st = m.wait()
         if world > 1:     # NCCL over NVLink only to gather embeddings + masks
             gather_rows([emb, masks.view(n_loc, -1)], counts)
@@ -409,7 +410,7 @@ def main():
         d2h = int(outs[0].size * 4 + outs[1].size)
 
         def hstep():
-            m.embed_async(xh.numpy(), ch.numpy(), plan, out=outs, stream=stream)
+            m.embed_async(xh.numpy(), ch.numpy(), plan, out=outs, stream=stream, x_bf16=args.x_bf16)
             return m.wait()
         hstep()
         torch.cuda.synchronize()
@@ -432,7 +433,7 @@ def main():
             ss = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
             pouts = [outs, host_outs()]
             for k in range(2):          # warm-up: capture each context's graph
-                ctxs[k].embed_async(xh.numpy(), ch.numpy(), plan, out=pouts[k], stream=ss[k])
+                ctxs[k].embed_async(xh.numpy(), ch.numpy(), plan, out=pouts[k], stream=ss[k], x_bf16=args.x_bf16)
                 ctxs[k].wait()
             torch.cuda.synchronize()
             if world > 1:
@@ -441,7 +442,8 @@ def main():
             p0.record(ss[0])
             ss[1].wait_event(p0)
             for k in range(args.steps):
-                ctxs[k % 2].embed_async(xh.numpy(), ch.numpy(), plan, out=pouts[k % 2], stream=ss[k % 2])
+                ctxs[k % 2].embed_async(xh.numpy(), ch.numpy(), plan, out=pouts[k % 2], stream=ss[k % 2],
+                                        x_bf16=args.x_bf16)
                 if k >= 1:
                     ctxs[(k - 1) % 2].wait()
             ctxs[(args.steps - 1) % 2].wait()
@@ -546,7 +548,8 @@ def main():
             "config": {"workload": wl["desc"], "model": f"{args.config if args.workload != 'c5' else 'l14_336'} "
                                                         "(random init) + structured gates",
                        "seq_len": T, **wl["config_extra"],
-                       "compute": "bf16 operands, fp32 accumulate, fp32 residual",
+                       "compute": "bf16 operands, fp32 accumulate, "
+                                  + ("bf16 residual stream (RV_X_BF16)" if args.x_bf16 else "fp32 residual"),
                        "variant": "SPEC chain (RV_CHAIN)" if args.chain else "D1 layer-gated (default)"},
             "reuse": {"reuse_all": stats["reuse_all"], "reuse_nonI": stats["reuse_nonI"]},
             "waves": waves_info,

@@ -118,6 +118,12 @@ typedef struct {
                               soon as wave (l, k-1) and wave (l-1, k) are done (wavefront over
                               rings of R layer buffers, one stream per wave index);
                               results are bitwise identical, only the concurrency differs        */
+#define RV_X_BF16 2048u    /* experimental: the residual stream X (every layer's input and
+                              output token rows, the reuse cache's X part) is stored in bf16 instead
+                              of fp32 — half the bytes of the score, LN1, residual and restoration
+                              traffic; LN statistics, the decision, the GEMM accumulators and the
+                              residual adds still compute in fp32 and round once on store.  D1 path
+                              only (RV_ECONTRACT with RV_CHAIN)                                  */
 #define RV_ATTN_SYNC 32u   /* diagnostic: attention on the mma.sync kernel (k_attn.cu) even where the
                               tcgen05/TMEM kernels (k_attn_tc.cu: d_h = 64) apply; without it the
                               mma.sync kernel runs only for d_h = 16 (the tiny config)            */

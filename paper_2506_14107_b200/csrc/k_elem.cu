@@ -14,12 +14,18 @@ namespace {
 
 constexpr int ROWS_PER_CTA = 8;  // 8 warps
 
-template <int VPL>
-RV_DEV void load_row(const float* __restrict__ src, int D, int lane, float (&x)[VPL]) {
+RV_DEV float to_f(float v) { return v; }
+RV_DEV float to_f(bf16 v) { return __bfloat162float(v); }
+RV_DEV void from_f(float& d, float v) { d = v; }
+RV_DEV void from_f(bf16& d, float v) { d = __float2bfloat16_rn(v); }
+
+// XT = float (fp32 residual stream) or bf16 (RV_X_BF16)
+template <int VPL, typename XT>
+RV_DEV void load_row(const XT* __restrict__ src, int D, int lane, float (&x)[VPL]) {
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int k = lane + 32 * j;
-    x[j] = k < D ? src[k] : 0.f;
+    x[j] = k < D ? to_f(src[k]) : 0.f;
   }
 }
 
@@ -56,8 +62,8 @@ __global__ void patch_to_bf16_kernel(const float* __restrict__ src, bf16* __rest
   }
 }
 
-template <int VPL>
-__global__ void embed_finish_kernel(float* __restrict__ X, const float* __restrict__ cls,
+template <int VPL, typename XT>
+__global__ void embed_finish_kernel(XT* __restrict__ X, const float* __restrict__ cls,
                                     const float* __restrict__ pos, const float* __restrict__ g,
                                     const float* __restrict__ b, float* __restrict__ pclsh, int n,
                                     int T, int D, int N, int H) {
@@ -66,7 +72,7 @@ __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restri
   for (long long r = blockIdx.x * (long long)ROWS_PER_CTA + warp; r < rows;
        r += (long long)gridDim.x * ROWS_PER_CTA) {
     const int tok = (int)(r % T);
-    float* row = X + r * D;
+    XT* row = X + r * D;
     float x[VPL];
     if (tok == 0) load_row<VPL>(cls, D, lane, x);
     else load_row<VPL>(row, D, lane, x);          // patches @ W_pe written by the PE GEMM
@@ -78,7 +84,7 @@ __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restri
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int k = lane + 32 * j;
-      if (k < D) row[k] = x[j];
+      if (k < D) from_f(row[k], x[j]);
     }
     if (tok > 0 && lane < H) pclsh[((r / T) * H + lane) * N + (tok - 1)] = 1.0f / (float)N;  // layer-1 t
   }
@@ -91,8 +97,8 @@ __global__ void embed_finish_kernel(float* __restrict__ X, const float* __restri
 #ifndef RV_LN_MINB
 #define RV_LN_MINB 3
 #endif
-template <int VPL>
-__global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_kernel(const float* __restrict__ src, const int* __restrict__ rows,
+template <int VPL, typename XT>
+__global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_kernel(const XT* __restrict__ src, const int* __restrict__ rows,
                                  const int* __restrict__ count, int M_host, const float* __restrict__ g,
                                  const float* __restrict__ b, bf16* __restrict__ dst, int D) {
   const int M = count ? *count : M_host;
@@ -116,18 +122,28 @@ __global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_kernel(const float*
 #ifndef RV_LN_VEC
 #define RV_LN_VEC 1
 #endif
-template <int V4>
-__global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_vec_kernel(const float* __restrict__ src, const int* __restrict__ rows,
+template <int V4, typename XT>
+__global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_vec_kernel(const XT* __restrict__ src, const int* __restrict__ rows,
                                      const int* __restrict__ count, int M_host, const float* __restrict__ g,
                                      const float* __restrict__ b, bf16* __restrict__ dst, int D) {
   const int M = count ? *count : M_host;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int m = blockIdx.x * ROWS_PER_CTA + warp; m < M; m += gridDim.x * ROWS_PER_CTA) {
     const long long r = rows ? rows[m] : m;
-    const float4* s4 = reinterpret_cast<const float4*>(src + r * D);
     float4 x[V4];
+    if constexpr (sizeof(XT) == 4) {
+      const float4* s4 = reinterpret_cast<const float4*>(src + r * D);
 #pragma unroll
-    for (int j = 0; j < V4; ++j) x[j] = s4[lane + 32 * j];
+      for (int j = 0; j < V4; ++j) x[j] = s4[lane + 32 * j];
+    } else {   // bf16 row: 8 B per 4 columns
+      const uint2* s2 = reinterpret_cast<const uint2*>(src + r * D);
+#pragma unroll
+      for (int j = 0; j < V4; ++j) {
+        const uint2 u = s2[lane + 32 * j];
+        const float2 lo = unpack_bf16x2(u.x), hi = unpack_bf16x2(u.y);
+        x[j] = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+    }
     float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < V4; ++j) sum += (x[j].x + x[j].y) + (x[j].z + x[j].w);
@@ -150,8 +166,8 @@ __global__ void __launch_bounds__(256, RV_LN_MINB) gather_ln_vec_kernel(const fl
   }
 }
 
-template <int VPL>
-__global__ void ln_post_kernel(const float* __restrict__ X, const float* __restrict__ g,
+template <int VPL, typename XT>
+__global__ void ln_post_kernel(const XT* __restrict__ X, const float* __restrict__ g,
                                const float* __restrict__ b, float* __restrict__ emb, int n, int T,
                                int D) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -207,41 +223,56 @@ cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g,
+cudaError_t launch_embed_finish(void* X, int x_bf16, const float* cls, const float* pos, const float* g,
                                 const float* b, float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s) {
   const int grid = grid_rows((long long)n * T);
   const int v = (D + 31) / 32;
-  if (v <= 2) embed_finish_kernel<2><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
-  else if (v <= 24) embed_finish_kernel<24><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
-  else embed_finish_kernel<32><<<grid, 256, 0, s>>>(X, cls, pos, g, b, pclsh, n, T, D, N, H);
+#define RV_EF(V, XT) embed_finish_kernel<V, XT><<<grid, 256, 0, s>>>(reinterpret_cast<XT*>(X), cls, pos, g, b, pclsh, n, T, D, N, H)
+  if (x_bf16) {
+    if (v <= 2) RV_EF(2, bf16); else if (v <= 24) RV_EF(24, bf16); else RV_EF(32, bf16);
+  } else {
+    if (v <= 2) RV_EF(2, float); else if (v <= 24) RV_EF(24, float); else RV_EF(32, float);
+  }
+#undef RV_EF
   return cudaGetLastError();
 }
 
-cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
-                             const float* g, const float* b, bf16* dst, int D, cudaStream_t s) {
+template <typename XT>
+cudaError_t gather_ln_t(const XT* src, const int* rows, const int* count, int M_host, int max_rows,
+                        const float* g, const float* b, bf16* dst, int D, cudaStream_t s) {
   const int grid = grid_rows(max_rows);
   const int v = (D + 31) / 32;
   if (RV_LN_VEC && D == 1024) {
-    gather_ln_vec_kernel<8><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+    gather_ln_vec_kernel<8, XT><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
     return cudaGetLastError();
   }
   if (RV_LN_VEC && D == 768) {
-    gather_ln_vec_kernel<6><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+    gather_ln_vec_kernel<6, XT><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
     return cudaGetLastError();
   }
-  if (v <= 2) gather_ln_kernel<2><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
-  else if (v <= 24) gather_ln_kernel<24><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
-  else gather_ln_kernel<32><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  if (v <= 2) gather_ln_kernel<2, XT><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  else if (v <= 24) gather_ln_kernel<24, XT><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
+  else gather_ln_kernel<32, XT><<<grid, 256, 0, s>>>(src, rows, count, M_host, g, b, dst, D);
   return cudaGetLastError();
 }
 
-cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
+cudaError_t launch_gather_ln(const void* src, int src_bf16, const int* rows, const int* count, int M_host,
+                             int max_rows, const float* g, const float* b, bf16* dst, int D, cudaStream_t s) {
+  if (src_bf16) return gather_ln_t(reinterpret_cast<const bf16*>(src), rows, count, M_host, max_rows, g, b, dst, D, s);
+  return gather_ln_t(reinterpret_cast<const float*>(src), rows, count, M_host, max_rows, g, b, dst, D, s);
+}
+
+cudaError_t launch_ln_post(const void* X, int x_bf16, const float* g, const float* b, float* emb, int n, int T, int D,
                            cudaStream_t s) {
   const int grid = grid_rows(n);
   const int v = (D + 31) / 32;
-  if (v <= 2) ln_post_kernel<2><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
-  else if (v <= 24) ln_post_kernel<24><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
-  else ln_post_kernel<32><<<grid, 256, 0, s>>>(X, g, b, emb, n, T, D);
+#define RV_LP(V, XT) ln_post_kernel<V, XT><<<grid, 256, 0, s>>>(reinterpret_cast<const XT*>(X), g, b, emb, n, T, D)
+  if (x_bf16) {
+    if (v <= 2) RV_LP(2, bf16); else if (v <= 24) RV_LP(24, bf16); else RV_LP(32, bf16);
+  } else {
+    if (v <= 2) RV_LP(2, float); else if (v <= 24) RV_LP(24, float); else RV_LP(32, float);
+  }
+#undef RV_LP
   return cudaGetLastError();
 }
 

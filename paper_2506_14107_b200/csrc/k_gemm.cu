@@ -358,9 +358,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int rr = i * 4 + rsub;
-          x[i] = (rr < nvalid && orow_s[rr] >= 0) ? *reinterpret_cast<const float4*>(e.resid + (long long)rrow_s[rr] * e.resid_ld +
-                                                                nb * BN + c * 32 + c4)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          const long long off = (long long)rrow_s[rr] * e.resid_ld + nb * BN + c * 32 + c4;
+          if (!(rr < nvalid && orow_s[rr] >= 0)) {
+            x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else if (e.resid_bf16) {
+            const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.resid) + off);
+            const float2 lo = unpack_bf16x2(u.x), hi = unpack_bf16x2(u.y);
+            x[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
+          } else {
+            x[i] = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.resid) + off);
+          }
         }
       };
       // SR: this lane's 8 x 16 B of chunk c go to ring slot c % RDEPTH (read back by the same
@@ -373,11 +380,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
             const int rr = i * 4 + rsub;
             const bool live = rr < nvalid && orow_s[rr] >= 0;
             const int rrow = __shfl_sync(0xffffffffu, rrow_reg, live ? rr : 0);
-            const float* src = e.resid + (long long)rrow * e.resid_ld + nb * BN + c * 32 + c4;
+            const long long off = (long long)rrow * e.resid_ld + nb * BN + c * 32 + c4;
             const uint32_t dst = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                         "r"(live ? 16 : 0)
-                         : "memory");
+            if (e.resid_bf16)   // 4 bf16 = 8 B into the first half of the lane's 16 B chunk
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
+                           "l"(reinterpret_cast<const bf16*>(e.resid) + off), "r"(live ? 8 : 0)
+                           : "memory");
+            else
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                           "l"(reinterpret_cast<const float*>(e.resid) + off), "r"(live ? 16 : 0)
+                           : "memory");
           }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");   // one group per chunk slot (maybe empty)
@@ -400,7 +412,15 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int rr = i * 4 + rsub;
-              xc[i] = lds128(ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4));
+              const uint32_t a = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
+              if (e.resid_bf16) {
+                uint32_t u0, u1;
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(u0), "=r"(u1) : "r"(a) : "memory");
+                const float2 lo = unpack_bf16x2(u0), hi = unpack_bf16x2(u1);
+                xc[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
+              } else {
+                xc[i] = lds128(a);
+              }
             }
           }
           // the slot's residual is in registers: it now serves as this chunk's transpose tile

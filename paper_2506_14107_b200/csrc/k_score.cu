@@ -35,9 +35,17 @@ constexpr int SCORE_TOK = 64;
 #ifndef RV_SCORE_MINB
 #define RV_SCORE_MINB 3
 #endif
-template <int VPL>
+// 4 consecutive elements 4 k4 .. 4 k4 + 3 of a residual-stream row (fp32, or bf16: RV_X_BF16)
+RV_DEV float4 ld4(const float* __restrict__ row, int k4) { return __ldg(reinterpret_cast<const float4*>(row) + k4); }
+RV_DEV float4 ld4(const bf16* __restrict__ row, int k4) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(row) + k4);
+  const float2 lo = unpack_bf16x2(u.x), hi = unpack_bf16x2(u.y);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+template <int VPL, typename XT>
 __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
-    score_kernel(const float* __restrict__ X, int T, int D, int N, int L, int layer,
+    score_kernel(const XT* __restrict__ X, int T, int D, int N, int L, int layer,
                  const int4* __restrict__ wdesc, const float* __restrict__ tsrc, int tH,
                  const float* __restrict__ codec, const uint8_t* force,
                  const float* __restrict__ gate, int Hg, int dense, uint8_t* masks, float* scores,
@@ -82,19 +90,19 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
   const int D4 = D >> 2;
   int my_reused = 0;
   for (int i = i_beg + warp; i <= i_end; i += SCORE_THREADS / 32) {
-    const float4* cur = reinterpret_cast<const float4*>(X + ((long long)slot * T + i) * D);
-    const float4* rp = past >= 0 ? reinterpret_cast<const float4*>(X + ((long long)past * T + i) * D) : nullptr;
-    const float4* rf = fut >= 0 ? reinterpret_cast<const float4*>(X + ((long long)fut * T + i) * D) : nullptr;
+    const XT* cur = X + ((long long)slot * T + i) * D;
+    const XT* rp = past >= 0 ? X + ((long long)past * T + i) * D : nullptr;
+    const XT* rf = fut >= 0 ? X + ((long long)fut * T + i) * D : nullptr;
     float cc = 0.f, pp = 0.f, ff = 0.f, cp = 0.f, cf = 0.f;
     if constexpr (VPL > 0) {
-      const float4* rp2 = rp ? rp : cur;
-      const float4* rf2 = rf ? rf : cur;
+      const XT* rp2 = rp ? rp : cur;
+      const XT* rf2 = rf ? rf : cur;
       float4 cv[VPL], pv[VPL], fv[VPL];
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        cv[j] = __ldg(cur + lane + 32 * j);
-        pv[j] = __ldg(rp2 + lane + 32 * j);
-        fv[j] = __ldg(rf2 + lane + 32 * j);
+        cv[j] = ld4(cur, lane + 32 * j);
+        pv[j] = ld4(rp2, lane + 32 * j);
+        fv[j] = ld4(rf2, lane + 32 * j);
       }
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
@@ -110,15 +118,15 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
     } else
 #pragma unroll 4
     for (int k = lane; k < D4; k += 32) {
-      const float4 c = __ldg(cur + k);
+      const float4 c = ld4(cur, k);
       cc += c.x * c.x + c.y * c.y + c.z * c.z + c.w * c.w;
       if (rp) {
-        const float4 p = __ldg(rp + k);
+        const float4 p = ld4(rp, k);
         pp += p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w;
         cp += c.x * p.x + c.y * p.y + c.z * p.z + c.w * p.w;
       }
       if (rf) {
-        const float4 f = __ldg(rf + k);
+        const float4 f = ld4(rf, k);
         ff += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
         cf += c.x * f.x + c.y * f.y + c.z * f.z + c.w * f.w;
       }
@@ -159,11 +167,11 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
     if (M && dfull) {
       // Eq. 8: Delta R_i = R_cur_i - R_ref_i, written now while both rows are cache-hot, to
       // the wave-local token row w*T + i: the restoration GEMM reads it there in place
-      const float4* rr = prov ? rf : rp;
+      const XT* rr = prov ? rf : rp;
       uint2* o = reinterpret_cast<uint2*>(dfull + ((long long)w * T + i) * D);
 #pragma unroll 4
       for (int k = lane; k < D4; k += 32) {
-        const float4 a = __ldg(cur + k), b = __ldg(rr + k);
+        const float4 a = ld4(cur, k), b = ld4(rr, k);
         uint2 u;
         u.x = pack_bf16x2(a.x - b.x, a.y - b.y);
         u.y = pack_bf16x2(a.z - b.z, a.w - b.w);
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
 
 }  // namespace
 
-cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
+cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
                          int* cntR, bf16* dfull, cudaStream_t s) {
@@ -274,12 +282,19 @@ cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, 
   while (tok > SCORE_THREADS / 32 && (long long)n_w * ((N + tok - 1) / tok) < 3LL * dev_sms()) tok >>= 1;
   dim3 grid(n_w, (N + tok - 1) / tok);
   const int4* wd = reinterpret_cast<const int4*>(wdesc);
-#define RV_SCORE(V)                                                                                              \
-  score_kernel<V><<<grid, SCORE_THREADS, 0, s>>>(X, T, D, N, L, layer, wd, tsrc, tH, codec, force, gate, Hg, dense, \
-                                                 masks, scores, wmask, wprov, cntR, dfull, tok)
-  if (D == 1024) RV_SCORE(8);
-  else if (D == 768) RV_SCORE(6);
-  else RV_SCORE(0);
+#define RV_SCORE(V, XT)                                                                                         \
+  score_kernel<V, XT><<<grid, SCORE_THREADS, 0, s>>>(reinterpret_cast<const XT*>(X), T, D, N, L, layer, wd, tsrc, tH, \
+                                                     codec, force, gate, Hg, dense, masks, scores, wmask, wprov, cntR, \
+                                                     dfull, tok)
+  if (x_bf16) {
+    if (D == 1024) RV_SCORE(8, bf16);
+    else if (D == 768) RV_SCORE(6, bf16);
+    else RV_SCORE(0, bf16);
+  } else {
+    if (D == 1024) RV_SCORE(8, float);
+    else if (D == 768) RV_SCORE(6, float);
+    else RV_SCORE(0, float);
+  }
 #undef RV_SCORE
   return cudaGetLastError();
 }

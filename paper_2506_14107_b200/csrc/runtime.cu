@@ -599,6 +599,9 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   const cudaStream_t s0 = s;   // the embed stream (wave streams fork from and join into it)
   const bool dense = flags & RV_DENSE;
   const bool force = flags & RV_FORCE_MASKS;
+  // RV_X_BF16: the residual stream X (every layer's input/output rows) is stored in bf16; the X
+  // buffers keep their fp32 size and hold the bf16 rows in their first half-rows
+  const int xb = (flags & RV_X_BF16) ? 1 : 0;
   r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
   --r.launches;
   // a1: patch embed (dense, all frames): bf16 operand, GEMM into X0 rows f*T+1+i, finish.
@@ -608,20 +611,21 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
     Epi e;
     e.out = ctx->X[0];
     e.out_ld = D;
+    e.out_bf16 = xb;
     e.row_div = N;
     e.row_add = 1;
     r.begin(K_PE,-1,-1);
     r.chk(gemm_launch(ctx->pe, nullptr, n * N, n * N, e, s), "gemm_pe");
   }
   r.begin(K_EMBED,-1,-1);
-  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
+  r.chk(launch_embed_finish(ctx->X[0], xb, ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
         "embed_finish");
   const bool keepall = ctx->keepall;
   const size_t nTD = (size_t)ctx->n_cap * T * D;
   const int R = ctx->wf_R;                 // >= 3: wavefront schedule over rings of layer buffers
   const int nwv = (int)ctx->waves.size();
   // X_l (input of layer l + 1), K/V_l and the source-row table of layer l
-  auto Xbuf = [&](int l) -> float* {
+  auto Xbuf = [&](int l) -> float* {   // (bf16 rows with RV_X_BF16: same base, half the row stride)
     return keepall ? ctx->Xall + (size_t)l * nTD : (R ? ctx->Xr[l % R] : ctx->X[l & 1]);
   };
   auto KVbuf = [&](int l) -> bf16* {
@@ -680,7 +684,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       }
       // a2-a3: Eq. 1-4
       r.begin(K_SCORE,l,wi);
-      r.chk(launch_score(Xin, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
+      r.chk(launch_score(Xin, xb, T, D, N, L, l, n_w, wd, ctx->pclsh, H, codec, force ? masks : nullptr,
                          ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, b.wmask,
                          b.wprov, b.cntR, b.dfull, s),
             "score");
@@ -693,7 +697,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       const int* MC = b.counts;
       // a5: gather + LN1
       r.begin(K_GATHER,l,wi);
-      r.chk(launch_gather_ln(Xin, b.idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, b.A, D, s), "gather_ln1");
+      r.chk(launch_gather_ln(Xin, xb, b.idxC, MC, 0, maxC, w.ln1_g, w.ln1_b, b.A, D, s), "gather_ln1");
       // a6: QKV; q compact, K/V scattered to the cache rows of C
       {
         Epi e;
@@ -729,6 +733,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.resid = Xin;
         e.resid_rows = b.idxC;
         e.resid_ld = D;
+        e.resid_bf16 = xb;
         e.out = b.x1;
         e.out_ld = D;
         r.begin(K_WO,l,wi);
@@ -736,7 +741,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       }
       // a10: LN2 + FC1 + QuickGELU
       r.begin(K_LN2,l,wi);
-      r.chk(launch_gather_ln(b.x1, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, b.A, D, s), "ln2");
+      r.chk(launch_gather_ln(b.x1, 0, nullptr, MC, 0, maxC, w.ln2_g, w.ln2_b, b.A, D, s), "ln2");
       {
         Epi e;
         e.bias = w.b1;
@@ -756,6 +761,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e.out = Xout;
         e.out_rows = b.idxC;
         e.out_ld = D;
+        e.out_bf16 = xb;
         r.begin(K_FC2,l,wi);
         r.chk(gemm_launch(plan(ctx->g_fc2[l], b, b.tmH), MC, 0, maxC, e, s), "gemm_fc2");
       }
@@ -778,9 +784,11 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
         e2.resid = Xout;
         e2.resid_rows = b.provrow;
         e2.resid_ld = D;
+        e2.resid_bf16 = xb;
         e2.out = Xout;
         e2.out_rows = b.idxR;
         e2.out_ld = D;
+        e2.out_bf16 = xb;
         r.begin(K_R2,l,wi);
         r.chk(gemm_launch(plan(ctx->g_r2[l], b, b.tmHr), b.counts + 1, 0, n_w * N, e2, s), "gemm_r2");
       }
@@ -799,7 +807,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   }
   // a14: Z = LN_post(CLS), slots are display indices
   r.begin(K_LNPOST,-1,-1);
-  r.chk(launch_ln_post(Xbuf(L), ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
+  r.chk(launch_ln_post(Xbuf(L), xb, ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
 }
 
 // SPEC chain variant (RV_CHAIN; oracle/chain_ref.py):
@@ -830,7 +838,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
   }
   // embed_finish also writes the uniform t of the first decision into ctx->pclsh (= P[1])
   r.begin(K_EMBED,-1,-1);
-  r.chk(launch_embed_finish(ctx->X[0], ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
+  r.chk(launch_embed_finish(ctx->X[0], 0, ctx->cls, ctx->pos, ctx->lnpre_g, ctx->lnpre_b, ctx->pclsh, n, T, D, N, H, s),
         "embed_finish");
   float* P[2] = {ctx->pcl2, ctx->pclsh};       // attention of layer l writes P[l & 1]
   int* KS[2] = {ctx->kvsrc, ctx->kvsrc2};      // source rows of layer l's q|k|v: KS[l & 1]
@@ -840,7 +848,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
     const int rows = wv.n_w * T;
     const int* wr = ctx->wrows + (size_t)wv.off * T;
     r.begin(K_GATHER,0,wi);
-    r.chk(launch_gather_ln(ctx->X[0], wr, nullptr, rows, rows, ctx->lw[0].ln1_g, ctx->lw[0].ln1_b, ctx->A, D, s),
+    r.chk(launch_gather_ln(ctx->X[0], 0, wr, nullptr, rows, rows, ctx->lw[0].ln1_g, ctx->lw[0].ln1_b, ctx->A, D, s),
           "gather_ln1");
     Epi e;
     e.bias = ctx->lw[0].bqkv;
@@ -894,7 +902,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       }
       // decision on x' (Eq. 1-4), t = the previous layer's CLS attention
       r.begin(K_SCORE,l,wi);
-      r.chk(launch_score(ctx->XP, T, D, N, L, l, n_w, wd, P[(l + 1) & 1], H, codec, force ? masks : nullptr,
+      r.chk(launch_score(ctx->XP, 0, T, D, N, L, l, n_w, wd, P[(l + 1) & 1], H, codec, force ? masks : nullptr,
                          ctx->gates_loaded ? w.gate : nullptr, ctx->Hg, dense ? 1 : 0, masks, scores, ctx->wmask,
                          ctx->wprov, ctx->cntR, ctx->dfull, s),
             "score");
@@ -907,7 +915,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       const int* MC = ctx->counts;
       // chain FFN_l on C: LN2(x') -> FC1 -> FC2 + x', scattered to X_l rows
       r.begin(K_LN2,l,wi);
-      r.chk(launch_gather_ln(ctx->XP, ctx->idxC, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
+      r.chk(launch_gather_ln(ctx->XP, 0, ctx->idxC, MC, 0, maxC, w.ln2_g, w.ln2_b, ctx->A, D, s), "ln2");
       {
         Epi e;
         e.bias = w.b1;
@@ -956,7 +964,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       if (l + 1 < L) {
         const LayerW& wn = ctx->lw[l + 1];
         r.begin(K_GATHER,l + 1,wi);
-        r.chk(launch_gather_ln(Xout, ctx->idxC, MC, 0, maxC, wn.ln1_g, wn.ln1_b, ctx->A, D, s), "gather_ln1");
+        r.chk(launch_gather_ln(Xout, 0, ctx->idxC, MC, 0, maxC, wn.ln1_g, wn.ln1_b, ctx->A, D, s), "gather_ln1");
         Epi e;
         e.bias = wn.bqkv;
         e.out = Qn + 2 * D;
@@ -974,7 +982,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
     }
   }
   r.begin(K_LNPOST,-1,-1);
-  r.chk(launch_ln_post(ctx->X[L & 1], ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
+  r.chk(launch_ln_post(ctx->X[L & 1], 0, ctx->lnpost_g, ctx->lnpost_b, emb, n, T, D, s), "ln_post");
 }
 
 rv_status ensure_chain_buffers(rv_ctx* ctx, int n) {
@@ -1252,6 +1260,8 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   if (total_desc != n) return fail(ctx, RV_EPLAN, "rv_embed: internal wave bookkeeping mismatch");
   const bool keepall = flags & RV_KEEP_ALL_CACHE;
   if (keepall && (flags & RV_CHAIN)) return fail(ctx, RV_ECONTRACT, "rv_embed: RV_KEEP_ALL_CACHE is a D1-path ablation");
+  if ((flags & RV_X_BF16) && (flags & RV_CHAIN))
+    return fail(ctx, RV_ECONTRACT, "rv_embed: RV_X_BF16 is implemented for the D1 path only");
   if ((st = ensure_buffers(ctx, n, (long long)max_w * T, any_ref_all ? (long long)max_w * N : 0, max_w, keepall)))
     return st;
   // Wavefront schedule when the level waves are too small to fill the GPU and the
@@ -1416,8 +1426,10 @@ rv_status rv_wait(rv_ctx* ctx, rv_stats* stats) {
       flops += (double)n * T * (4 * T * D + 2 * D * D) + c * (4 * D * F + (l + 1 < L ? 6 * D * D : 0.0)) + r * per_r;
     else
       flops += c * per_c + r * per_r;
-    // algorithmic bytes: 60 D per recomputed token-layer, 18 D per reused one
-    bytes += c * 60.0 * D + r * 18.0 * D;
+    // algorithmic bytes: 60 D per recomputed token-layer, 18 D per reused one;
+    // RV_X_BF16 halves their X-row parts (16 D and 12 D): 52 D and 12 D
+    if (ctx->cur_flags & RV_X_BF16) bytes += c * 52.0 * D + r * 12.0 * D;
+    else bytes += c * 60.0 * D + r * 18.0 * D;
     stats->reuse_by_layer[l] = ctx->cur_nonI ? (float)(r / ((double)ctx->cur_nonI * N)) : 0.f;
   }
   stats->reuse_nonI = ctx->cur_nonI ? reused / ((double)ctx->cur_nonI * L * N) : 0.0;
@@ -1522,23 +1534,25 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
           MC = r.l == 0 ? nw * T : log[((size_t)(r.l - 1) * nwv + r.w) * 2];
       }
     }
-    // Algorithmic FLOPs (tensor work) and HBM bytes of this launch.
+    // Algorithmic FLOPs (tensor work) and HBM bytes of this launch; xs = bytes
+    // per element of the residual stream X (4, or 2 with RV_X_BF16)
+    const double xs = (ctx->cur_flags & RV_X_BF16) ? 2.0 : 4.0;
     switch (r.cls) {
       case K_PATCH: a.bytes += n * N * (ctx->pp * 4.0 + ctx->KP * 2.0); break;
-      case K_PE: a.flops += 2.0 * n * N * ctx->pp * D; a.bytes += n * N * (ctx->KP * 2.0 + D * 4.0); break;
-      case K_EMBED: a.bytes += n * T * D * 8.0; break;
-      case K_SCORE: a.bytes += (wdec[r.w] + wrefs[r.w]) * N * D * 4.0 + wdec[r.w] * N * 10.0 + MR * D * 2.0; break;
+      case K_PE: a.flops += 2.0 * n * N * ctx->pp * D; a.bytes += n * N * (ctx->KP * 2.0 + D * xs); break;
+      case K_EMBED: a.bytes += n * T * D * 2.0 * xs; break;
+      case K_SCORE: a.bytes += (wdec[r.w] + wrefs[r.w]) * N * D * xs + wdec[r.w] * N * 10.0 + MR * D * 2.0; break;
       case K_COMPACT: a.bytes += nw * T * 2.0 + (MC + 2 * MR) * 4.0; break;
-      case K_GATHER: a.bytes += MC * (D * 4.0 + D * 2.0 + 4.0); break;
+      case K_GATHER: a.bytes += MC * (D * xs + D * 2.0 + 4.0); break;
       case K_QKV: a.flops += 2.0 * MC * 3 * D * D; a.bytes += MC * (D * 2.0 + 3 * D * 2.0) + 3 * D * D * 2.0; break;
       case K_ATTN: a.flops += 4.0 * MC * T * D; a.bytes += MC * D * 4.0 + nw * T * 2 * D * 2.0; break;
-      case K_WO: a.flops += 2.0 * MC * D * D; a.bytes += MC * (D * 2.0 + D * 4.0 + D * 4.0) + D * D * 2.0; break;
+      case K_WO: a.flops += 2.0 * MC * D * D; a.bytes += MC * (D * 2.0 + D * xs + D * 4.0) + D * D * 2.0; break;
       case K_LN2: a.bytes += MC * (D * 4.0 + D * 2.0); break;
       case K_FC1: a.flops += 2.0 * MC * F * D; a.bytes += MC * (D * 2.0 + F * 2.0) + F * D * 2.0; break;
-      case K_FC2: a.flops += 2.0 * MC * D * F; a.bytes += MC * (F * 2.0 + D * 4.0 + D * 4.0) + F * D * 2.0; break;
+      case K_FC2: a.flops += 2.0 * MC * D * F; a.bytes += MC * (F * 2.0 + D * 4.0 + D * xs) + F * D * 2.0; break;
       case K_R1: a.flops += 2.0 * MR * Hr * D; a.bytes += MR * (D * 2.0 + Hr * 2.0) + Hr * D * 2.0; break;
-      case K_R2: a.flops += 2.0 * MR * D * Hr; a.bytes += MR * (Hr * 2.0 + D * 4.0 * 2) + Hr * D * 2.0; break;
-      case K_LNPOST: a.bytes += n * D * 8.0; break;
+      case K_R2: a.flops += 2.0 * MR * D * Hr; a.bytes += MR * (Hr * 2.0 + D * xs * 2) + Hr * D * 2.0; break;
+      case K_LNPOST: a.bytes += n * D * (xs + 4.0); break;
     }
   }
   int k = 0;
@@ -1555,7 +1569,7 @@ rv_status rv_stage_score(rv_ctx* ctx, int32_t layer, const float* X, int32_t n_w
   if (!ctx->gates_loaded) return fail(ctx, RV_ECONTRACT, "rv_stage_score: gates not loaded");
   if (layer < 0 || layer >= ctx->L || n_w < 0) return fail(ctx, RV_ECONTRACT, "rv_stage_score: bad layer/n_w");
   CK(cudaSetDevice(ctx->device));
-  CK(launch_score(X, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, 1, codec, force, ctx->lw[layer].gate,
+  CK(launch_score(X, 0, ctx->T, ctx->D, ctx->N, ctx->L, layer, n_w, wdesc, t, 1, codec, force, ctx->lw[layer].gate,
                   ctx->Hg, 0, masks, scores, wmask, wprov, cntR, nullptr, (cudaStream_t)stream));
   return RV_OK;
 }

@@ -10,16 +10,18 @@
 namespace rv {
 
 // ---------------------------------------------------------------- GEMM epilogue (k_gemm.cu)
-// out[orow(m)][n] = act(acc[m][n] + bias[n]) + resid[rrow(m)][n]   (fp32 residual)
+// out[orow(m)][n] = act(acc[m][n] + bias[n]) + resid[rrow(m)][n]   (fp32 residual, or bf16 with
+// resid_bf16: the RV_X_BF16 residual stream)
 // orow(m) = out_rows ? out_rows[m] : m + (row_div ? m / row_div : 0) + row_add; orow(m) < 0: row m
 // is computed but not stored (restoration GEMM R1 over the wave's token rows)
 // Columns n >= split go to out2 (column n - split) with rows out2_rows[m].
 struct Epi {
   const float* bias = nullptr;
   int act = 0;                 // 0 identity, 1 QuickGELU
-  const float* resid = nullptr;
+  const void* resid = nullptr;
   const int* resid_rows = nullptr;
   long long resid_ld = 0;
+  int resid_bf16 = 0;
   void* out = nullptr;
   const int* out_rows = nullptr;
   long long out_ld = 0;
@@ -52,15 +54,16 @@ cudaError_t gemm_launch(const GemmPlan& p, const int* M_dev, int M_host, int max
 // ---------------------------------------------------------------- row kernels (k_elem.cu)
 typedef __nv_bfloat16 bf16;
 cudaError_t launch_patch_to_bf16(const float* src, bf16* dst, long long rows, int pp, int KP, cudaStream_t s);
-cudaError_t launch_embed_finish(float* X, const float* cls, const float* pos, const float* g, const float* b,
-                                float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s);
-cudaError_t launch_gather_ln(const float* src, const int* rows, const int* count, int M_host, int max_rows,
-                             const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
-cudaError_t launch_ln_post(const float* X, const float* g, const float* b, float* emb, int n, int T, int D,
+// x_bf16 / src_bf16: the residual stream X is bf16 (RV_X_BF16) instead of fp32
+cudaError_t launch_embed_finish(void* X, int x_bf16, const float* cls, const float* pos, const float* g,
+                                const float* b, float* pclsh, int n, int T, int D, int N, int H, cudaStream_t s);
+cudaError_t launch_gather_ln(const void* src, int src_bf16, const int* rows, const int* count, int M_host,
+                             int max_rows, const float* g, const float* b, bf16* dst, int D, cudaStream_t s);
+cudaError_t launch_ln_post(const void* X, int x_bf16, const float* g, const float* b, float* emb, int n, int T, int D,
                            cudaStream_t s);
 
 // ---------------------------------------------------------------- decision + compaction (k_score.cu)
-cudaError_t launch_score(const float* X, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
+cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
                          int* cntR, bf16* dfull, cudaStream_t s);
