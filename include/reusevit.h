@@ -124,6 +124,9 @@ typedef struct {
                               traffic; LN statistics, the decision, the GEMM accumulators and the
                               residual adds still compute in fp32 and round once on store.  D1 path
                               only (RV_ECONTRACT with RV_CHAIN)                                  */
+#define RV_RESTORE_GEMMS 4096u /* diagnostic: restoration as the two GEMMs R1 (over all wave rows, hr to
+                              HBM) and R2 instead of the fused k_restore kernel (results bitwise
+                              equal; the fused kernel runs wherever Hr = 128 and D % 128 == 0)   */
 #define RV_ATTN_SYNC 32u   /* diagnostic: attention on the mma.sync kernel (k_attn.cu) even where the
                               tcgen05/TMEM kernels (k_attn_tc.cu: d_h = 64) apply; without it the
                               mma.sync kernel runs only for d_h = 16 (the tiny config)            */

@@ -19,7 +19,7 @@ STATUS = {0: "RV_OK", -1: "RV_ECONFIG", -2: "RV_ESHAPE", -3: "RV_EPLAN", -4: "RV
           -5: "RV_ECONTRACT", -6: "RV_ECUDA", -7: "RV_ENOMEM", -8: "RV_EBUSY"}
 RV_DEVICE_PTRS, RV_DENSE, RV_FORCE_MASKS, RV_NO_GRAPH, RV_PROFILE, RV_ATTN_SYNC, RV_WAVE_FRAME, RV_CHAIN = (
     1, 2, 4, 8, 16, 32, 64, 128)
-RV_NO_COMPACTION, RV_KEEP_ALL_CACHE, RV_SERIAL_WAVES, RV_X_BF16 = 256, 512, 1024, 2048
+RV_NO_COMPACTION, RV_KEEP_ALL_CACHE, RV_SERIAL_WAVES, RV_X_BF16, RV_RESTORE_GEMMS = 256, 512, 1024, 2048, 4096
 RV_I, RV_P, RV_B2, RV_B1 = 0, 1, 2, 3
 
 

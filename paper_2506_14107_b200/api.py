@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (RV_ATTN_SYNC, RV_CHAIN, RV_DENSE, RV_DEVICE_PTRS, RV_FORCE_MASKS, RV_KEEP_ALL_CACHE,
-                   RV_NO_COMPACTION, RV_NO_GRAPH, RV_PROFILE, RV_SERIAL_WAVES, RV_WAVE_FRAME, RV_X_BF16, RvConfig, RvKernelProf, RvPlan, RvStats,
+                   RV_NO_COMPACTION, RV_NO_GRAPH, RV_PROFILE, RV_SERIAL_WAVES, RV_WAVE_FRAME, RV_X_BF16, RV_RESTORE_GEMMS, RvConfig, RvKernelProf, RvPlan, RvStats,
                    check, load_library)
 
 __all__ = ["ReuseViT", "plan_gop", "plan_check", "vit_blob_floats", "gate_blob_floats"]
@@ -118,9 +118,11 @@ class ReuseViT:
                     want_scores: bool = False, stream=None, graph: bool = True, out=None,
                     profile: bool = False, attn_tc: bool = True,
                     per_frame_waves: bool = False, chain: bool = False, no_compaction: bool = False,
-                    keep_all_cache: bool = False, serial_waves: bool = False, x_bf16: bool = False):
+                    keep_all_cache: bool = False, serial_waves: bool = False, x_bf16: bool = False,
+                    restore_gemms: bool = False):
         """Enqueue one embed; returns a handle for ``wait``.  ``x_bf16``: experimental bf16
-        residual stream (RV_X_BF16).  ``out`` optionally supplies the
+        residual stream (RV_X_BF16).  ``restore_gemms``: diagnostic, restoration as two GEMMs
+        (RV_RESTORE_GEMMS) instead of the fused kernel.  ``out`` optionally supplies the
         output buffers (emb, masks, scores) to reuse across calls (same pointers -> the
         cached CUDA graph is replayed)."""
         import torch
@@ -134,7 +136,8 @@ class ReuseViT:
                  | (0 if attn_tc else RV_ATTN_SYNC)
                  | (RV_WAVE_FRAME if per_frame_waves else 0) | (RV_CHAIN if chain else 0)
                  | (RV_NO_COMPACTION if no_compaction else 0) | (RV_KEEP_ALL_CACHE if keep_all_cache else 0)
-                 | (RV_SERIAL_WAVES if serial_waves else 0) | (RV_X_BF16 if x_bf16 else 0))
+                 | (RV_SERIAL_WAVES if serial_waves else 0) | (RV_X_BF16 if x_bf16 else 0)
+                 | (RV_RESTORE_GEMMS if restore_gemms else 0))
         if force_masks is not None:
             flags |= RV_FORCE_MASKS
         if device_path:

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
                    const uint8_t* __restrict__ wprov, const int* __restrict__ cntR, int* __restrict__ idxC,
                    int* __restrict__ idxR, int* __restrict__ provrow, int* __restrict__ qoff,
                    int* __restrict__ counts, int* kvsrc, unsigned long long* reuse_ctr, int* count_log,
-                   int* __restrict__ rpos, int all_c) {
+                   int* __restrict__ rpos, int* __restrict__ rloc, int all_c) {
   __shared__ int s_part[COMPACT_THREADS / 32];
   __shared__ int s_wc[COMPACT_THREADS / 32], s_wr[COMPACT_THREADS / 32];
   __shared__ int s_base[2];
@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
       const int r = offR + pr + __popc(br & lt);
       const int prow = (pv[i] ? d4.z : d4.y) * T + i;
       if (rpos) rpos[(long long)w * T + i] = r;
+      if (rloc) rloc[r] = w * T + i;      // wave-local Delta row of reused token r (fused restoration)
       idxR[r] = slot * T + i;
       provrow[r] = prow;
       // reuse-cache read in place: K/V of a reused token = its provider's (already final,
@@ -301,11 +302,12 @@ cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, 
 
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s, int all_c) {
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, int* rloc, cudaStream_t s,
+                           int all_c) {
   if (n_w <= 0) return cudaSuccess;
   compact_kernel<<<n_w, COMPACT_THREADS, 0, s>>>(n_w, T, reinterpret_cast<const int4*>(wdesc), wmask, wprov,
                                                  cntR, idxC, idxR, provrow, qoff, counts, kvsrc, reuse_ctr, count_log,
-                                                 rpos, all_c);
+                                                 rpos, rloc, all_c);
   return cudaGetLastError();
 }
 

@@ -52,7 +52,7 @@ struct Wave {
 struct WaveBuf {
   uint8_t *wmask = nullptr, *wprov = nullptr;
   int *cntR = nullptr, *idxC = nullptr, *idxR = nullptr, *provrow = nullptr, *qoff = nullptr, *counts = nullptr,
-      *rpos = nullptr;
+      *rpos = nullptr, *rloc = nullptr;
   bf16 *A = nullptr, *q = nullptr, *att = nullptr, *h = nullptr, *hr = nullptr, *dfull = nullptr;
   float* x1 = nullptr;
   bool maps = false;
@@ -99,6 +99,9 @@ struct rv_ctx {
   int* kvsrc = nullptr;       // [n][T] K/V source row of every token (reuse cache read in place)
   bf16* dfull = nullptr;      // [max_w][T][D] Delta of reused tokens (wave-local token rows, bf16)
   int* rpos = nullptr;        // [max_w][T] compact restoration row of token w*T+i (-1: recomputed)
+  int* rloc = nullptr;        // [capR] wave-local Delta row w*T+i of compact reused row r (fused restoration)
+  std::vector<CUtensorMap> tmR1, tmR2;   // per layer: W_r1 / W_r2 boxes {64, 128} (k_restore.cu)
+  bool fused_restore = false;            // restore_supported(D, Hr): the fused kernel replaces R1 + R2
   bf16* patches_bf16 = nullptr;
   // host-pointer embeds only (no RV_DEVICE_PTRS): staging copies of the caller's host buffers
   int h_cap = 0, hs_cap = 0;
@@ -167,10 +170,10 @@ struct rv_ctx {
 };
 
 enum { K_PATCH, K_PE, K_EMBED, K_SCORE, K_COMPACT, K_GATHER, K_QKV, K_ATTN, K_WO, K_LN2,
-       K_FC1, K_FC2, K_R1, K_R2, K_LNPOST, K_NCLS };
+       K_FC1, K_FC2, K_R1, K_R2, K_LNPOST, K_RESTORE, K_NCLS };
 static const char* kClsName[K_NCLS] = {"patch_to_bf16", "gemm_pe", "embed_finish", "score", "compact",
                                        "gather_ln1", "gemm_qkv", "attention", "gemm_wo", "ln2", "gemm_fc1",
-                                       "gemm_fc2", "gemm_r1", "gemm_r2", "ln_post"};
+                                       "gemm_fc2", "gemm_r1", "gemm_r2", "ln_post", "restore"};
 
 namespace {
 
@@ -326,7 +329,7 @@ void release_buffers(rv_ctx* ctx) {
   ctx->X[0] = ctx->X[1] = nullptr; ctx->KV = nullptr; ctx->pclsh = nullptr; ctx->kvsrc = nullptr;
   ctx->Xall = nullptr; ctx->KVall = nullptr; ctx->keepall = false; ctx->tmKVl.clear();
   ctx->cache_bytes = ctx->alloc_bytes = 0;
-  ctx->dfull = nullptr; ctx->rpos = nullptr; ctx->patches_bf16 = nullptr; ctx->wdesc = nullptr;
+  ctx->dfull = nullptr; ctx->rpos = nullptr; ctx->rloc = nullptr; ctx->patches_bf16 = nullptr; ctx->wdesc = nullptr;
   ctx->wmask = ctx->wprov = nullptr;
   ctx->cntR = ctx->idxC = ctx->idxR = ctx->provrow = ctx->qoff = ctx->counts = nullptr;
   ctx->A = ctx->q = ctx->att = ctx->h = ctx->hr = nullptr; ctx->x1 = nullptr; ctx->reuse_ctr = nullptr;
@@ -368,6 +371,7 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
   AL(ctx->kvsrc, n * T);
   AL(ctx->dfull, (size_t)max_w * T * D);
   AL(ctx->rpos, max_w * T);
+  AL(ctx->rloc, capR);
   AL(ctx->patches_bf16, (size_t)n * N * ctx->KP);
   AL(ctx->wdesc, (size_t)n * 4);
   AL(ctx->wmask, max_w * T);
@@ -413,6 +417,10 @@ rv_status ensure_buffers(rv_ctx* ctx, int n, long long capC, long long capR, int
       ok = gemm_make_plan(&ctx->g_r1[l], ctx->dfull, max_w * T, w.Wr1, ctx->Hr, (int)D, e, sizeof e) &&
            gemm_make_plan(&ctx->g_r2[l], ctx->hr, capR, w.Wr2, (int)D, ctx->Hr, e, sizeof e);
   }
+  ctx->fused_restore = ctx->gates_loaded && restore_supported((int)D, ctx->Hr);
+  ctx->tmR1.resize(L); ctx->tmR2.resize(L);
+  for (int l = 0; ok && ctx->fused_restore && l < L; ++l)
+    ok = restore_make_maps(&ctx->tmR1[l], &ctx->tmR2[l], ctx->lw[l].Wr1, ctx->lw[l].Wr2, (int)D, ctx->Hr, e, sizeof e);
   if (!ok) {
     release_buffers(ctx);
     return fail(ctx, RV_ECUDA, "%s", e);
@@ -479,6 +487,7 @@ rv_status ensure_wavefront(rv_ctx* ctx, int R) {
     if (wi == 0) {
       b.wmask = ctx->wmask; b.wprov = ctx->wprov; b.cntR = ctx->cntR; b.idxC = ctx->idxC; b.idxR = ctx->idxR;
       b.provrow = ctx->provrow; b.qoff = ctx->qoff; b.counts = ctx->counts; b.rpos = ctx->rpos; b.A = ctx->A;
+      b.rloc = ctx->rloc;
       b.q = ctx->q; b.att = ctx->att; b.h = ctx->h; b.hr = ctx->hr; b.dfull = ctx->dfull; b.x1 = ctx->x1;
     } else {
       capC = (nwf * T + 127) / 128 * 128;
@@ -490,6 +499,7 @@ rv_status ensure_wavefront(rv_ctx* ctx, int R) {
       AL(b.qoff, nwf + 1);
       AL(b.counts, 2);
       AL(b.rpos, nwf * T);
+      AL(b.rloc, capR);
       AL(b.idxC, capC);
       AL(b.idxR, capR);
       AL(b.provrow, capR);
@@ -638,7 +648,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   WaveBuf shared;   // the serial schedule's wave buffers (tensor maps: the GEMM plans' own)
   shared.wmask = ctx->wmask; shared.wprov = ctx->wprov; shared.cntR = ctx->cntR; shared.idxC = ctx->idxC;
   shared.idxR = ctx->idxR; shared.provrow = ctx->provrow; shared.qoff = ctx->qoff; shared.counts = ctx->counts;
-  shared.rpos = ctx->rpos; shared.A = ctx->A; shared.q = ctx->q; shared.att = ctx->att; shared.h = ctx->h;
+  shared.rpos = ctx->rpos; shared.rloc = ctx->rloc; shared.A = ctx->A; shared.q = ctx->q; shared.att = ctx->att; shared.h = ctx->h;
   shared.hr = ctx->hr; shared.dfull = ctx->dfull; shared.x1 = ctx->x1;
   auto plan = [](const GemmPlan& p, const WaveBuf& b, const CUtensorMap& a) {
     GemmPlan q = p;
@@ -691,7 +701,8 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       // a4: Eq. 5-6 stream compaction
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, b.wmask, b.wprov, b.cntR, b.idxC, b.idxR, b.provrow, b.qoff, b.counts, kvsrc,
-                           ctx->reuse_ctr + l, ctx->count_log + ((size_t)l * nwv + wi) * 2, b.rpos, s,
+                           ctx->reuse_ctr + l, ctx->count_log + ((size_t)l * nwv + wi) * 2, b.rpos,
+                           (ctx->fused_restore && !(flags & RV_RESTORE_GEMMS)) ? b.rloc : nullptr, s,
                            (flags & RV_NO_COMPACTION) ? 1 : 0),
             "compact");
       const int* MC = b.counts;
@@ -768,8 +779,15 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
       // a12: restoration (Eq. 9) + merge (Eq. 10, R side).  The score pass wrote Delta (Eq. 8)
       // into the wave-local token rows w*T+i; R1 reads them in place over all n_w*T rows and
       // stores only the reused rows, compacted (row map rpos; -1 for C rows): no Delta copy.
-      // R2 runs over the M_R compact rows.
-      if (wv.any_ref && !dense) {
+      // R2 runs over the M_R compact rows.  Where restore_supported (every CLIP shape) both are
+      // one fused kernel over the M_R compact reused rows instead (k_restore.cu): Delta gathered
+      // by rloc, hr kept on chip, provider rows of X_l streamed in, restored rows scattered.
+      if (wv.any_ref && !dense && ctx->fused_restore && !(flags & RV_RESTORE_GEMMS)) {
+        r.begin(K_RESTORE,l,wi);
+        r.chk(launch_restore(ctx->tmR1[l], ctx->tmR2[l], b.dfull, b.rloc, b.provrow, b.idxR, b.counts + 1, n_w * N,
+                             w.br1, w.br2, Xout, xb, D, s),
+              "restore");
+      } else if (wv.any_ref && !dense) {
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;
@@ -910,7 +928,8 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
       r.begin(K_COMPACT,l,wi);
       r.chk(launch_compact(n_w, T, wd, ctx->wmask, ctx->wprov, ctx->cntR, ctx->idxC, ctx->idxR, ctx->provrow,
                            ctx->qoff, ctx->counts, KS[(l + 1) & 1], ctx->reuse_ctr + l,
-                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos, s),
+                           ctx->count_log + ((size_t)l * ctx->waves.size() + wi) * 2, ctx->rpos,
+                           (ctx->fused_restore && !(flags & RV_RESTORE_GEMMS)) ? ctx->rloc : nullptr, s),
             "compact");
       const int* MC = ctx->counts;
       // chain FFN_l on C: LN2(x') -> FC1 -> FC2 + x', scattered to X_l rows
@@ -938,8 +957,14 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
         r.begin(K_FC2,l,wi);
         r.chk(gemm_launch(ctx->g_fc2[l], MC, 0, maxC, e, s), "gemm_fc2");
       }
-      // restoration of the block output (Delta of the chain inputs, written by the score pass)
-      if (wv.any_ref && !dense) {
+      // restoration of the block output (Delta of the chain inputs, written by the score pass):
+      // the fused kernel where supported (as in the D1 path), else R1 + R2 GEMMs
+      if (wv.any_ref && !dense && ctx->fused_restore && !(flags & RV_RESTORE_GEMMS)) {
+        r.begin(K_RESTORE,l,wi);
+        r.chk(launch_restore(ctx->tmR1[l], ctx->tmR2[l], ctx->dfull, ctx->rloc, ctx->provrow, ctx->idxR, ctx->counts + 1,
+                             n_w * N, w.br1, w.br2, Xout, 0, D, s),
+              "restore");
+      } else if (wv.any_ref && !dense) {
         Epi e1;
         e1.bias = w.br1;
         e1.act = 1;
@@ -1553,6 +1578,10 @@ int32_t rv_profile(rv_ctx* ctx, rv_kernel_prof* out, int32_t max_entries) {
       case K_R1: a.flops += 2.0 * MR * Hr * D; a.bytes += MR * (D * 2.0 + Hr * 2.0) + Hr * D * 2.0; break;
       case K_R2: a.flops += 2.0 * MR * D * Hr; a.bytes += MR * (Hr * 2.0 + D * xs * 2) + Hr * D * 2.0; break;
       case K_LNPOST: a.bytes += n * D * (xs + 4.0); break;
+      case K_RESTORE:   // R1 + R2 tensor work; Delta row in, provider row in, restored row out
+        a.flops += 4.0 * MR * D * Hr;
+        a.bytes += MR * (D * 2.0 + D * xs * 2) + 2.0 * Hr * D * 2.0;
+        break;
     }
   }
   int k = 0;
@@ -1580,7 +1609,7 @@ rv_status rv_stage_compact(rv_ctx* ctx, int32_t n_w, const int32_t* wdesc, const
   if (!ctx) return RV_ECONTRACT;
   CK(cudaSetDevice(ctx->device));
   CK(launch_compact(n_w, ctx->T, wdesc, wmask, wprov, cntR, idxC, idxR, provrow, qoff, counts, nullptr, nullptr, nullptr,
-                    nullptr, (cudaStream_t)stream));
+                    nullptr, nullptr, (cudaStream_t)stream));
   return RV_OK;
 }
 

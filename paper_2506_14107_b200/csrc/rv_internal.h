@@ -69,8 +69,18 @@ cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, 
                          int* cntR, bf16* dfull, cudaStream_t s);
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
-                           unsigned long long* reuse_ctr, int* count_log, int* rpos, cudaStream_t s,
+                           unsigned long long* reuse_ctr, int* count_log, int* rpos, int* rloc, cudaStream_t s,
                            int all_c = 0);
+
+// ---------------------------------------------------------------- fused restoration (k_restore.cu)
+// Eq. 8-10 over the M_R = *M_dev compacted reused rows of a wave: X[idxR[r]] = X[provrow[r]] +
+// QuickGELU(dfull[rloc[r]] W_r1^T + b_r1) W_r2^T + b_r2 (X fp32, or bf16 with x_bf16); Hr = 128.
+bool restore_supported(int D, int Hr);
+bool restore_make_maps(CUtensorMap* tmW1, CUtensorMap* tmW2, const bf16* Wr1, const bf16* Wr2, int D, int Hr,
+                       char* err, size_t errlen);
+cudaError_t launch_restore(const CUtensorMap& tmW1, const CUtensorMap& tmW2, const bf16* dfull, const int* rloc,
+                           const int* provrow, const int* idxR, const int* M_dev, int max_rows, const float* br1,
+                           const float* br2, void* X, int x_bf16, int D, cudaStream_t s);
 
 // 2D bf16 tensor map, box {64 cols, box_rows}, SWIZZLE_128B (k_gemm.cu)
 bool make_tmap_bf16(CUtensorMap* m, const void* ptr, long long rows, int cols, int box_rows, char* err,
