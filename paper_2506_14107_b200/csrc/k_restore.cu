@@ -37,13 +37,26 @@ namespace {
 constexpr int RS_BM = 128;                 // reused rows per tile (MMA M)
 constexpr int RS_HR = 128;                 // restoration hidden width (R1 N, R2 K)
 constexpr int RS_NC = 128;                 // R2 output columns per accumulator chunk (MMA N)
-constexpr int RS_AST = 4;                  // Delta chunk ring stages
-constexpr int RS_WST = 4;                  // weight chunk ring slots
+#ifndef RS_AST_N
+#define RS_AST_N 4
+#endif
+#ifndef RS_KPS_N
+#define RS_KPS_N 1
+#endif
+#ifndef RS_WST_N
+#define RS_WST_N 4
+#endif
+#ifndef RS_RDEPTH_N
+#define RS_RDEPTH_N 2
+#endif
+constexpr int RS_AST = RS_AST_N;           // Delta ring stages
+constexpr int RS_KPS = RS_KPS_N;           // 64-column K chunks per Delta stage (128 B x RS_KPS per row)
+constexpr int RS_WST = RS_WST_N;           // weight chunk ring slots
 constexpr int RS_EPI = 8;                  // epilogue warps
-constexpr int RS_RDEPTH = 2;               // residual chunks in flight per epilogue warp
+constexpr int RS_RDEPTH = RS_RDEPTH_N;     // residual chunks in flight per epilogue warp
 constexpr int RS_THREADS = (4 + RS_EPI) * 32;
 constexpr uint32_t RS_CHUNK = 128 * 128;   // 128 rows x 128 B (one SWIZZLE_128B K-major block)
-constexpr uint32_t RS_OFF_W = RS_AST * RS_CHUNK;
+constexpr uint32_t RS_OFF_W = RS_AST * RS_KPS * RS_CHUNK;
 constexpr uint32_t RS_OFF_A2 = RS_OFF_W + RS_WST * RS_CHUNK;
 constexpr uint32_t RS_OFF_EPI = RS_OFF_A2 + 2 * RS_CHUNK;
 constexpr uint32_t RS_OFF_BAR = RS_OFF_EPI + RS_EPI * RS_RDEPTH * 4096;
@@ -148,23 +161,25 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
     // ==================================================================== Delta loaders
     // lane L of the 64: 16 B column chunk L % 8 of rows L / 8 + 8 i (i < 16) of every K chunk
     const int l64 = warp * 32 + lane;
-    const int c = l64 & 7, r0 = l64 >> 3;
+    // (RS_KPS chunks per stage: 8 RS_KPS lanes copy a row's 128 RS_KPS contiguous bytes)
+    constexpr int LPR = 8 * RS_KPS, RPP = 64 / LPR, NIT = RS_BM / RPP;
+    const int c16 = l64 % LPR, r0 = l64 / LPR, blk = c16 >> 3, c = c16 & 7;
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      int src[16];
+      int src[NIT];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int m = tile * RS_BM + r0 + 8 * i;
+      for (int i = 0; i < NIT; ++i) {
+        const int m = tile * RS_BM + r0 + RPP * i;
         src[i] = m < M ? __ldg(rloc + m) : -1;
       }
-      for (int kc = 0; kc < nk; ++kc) {
+      for (int kc = 0; kc < nk; kc += RS_KPS) {
         mbar_wait(&a_empty[s], ph ^ 1);
-        const uint32_t dst = base + s * RS_CHUNK;
+        const uint32_t dst = base + (s * RS_KPS + blk) * RS_CHUNK;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r = r0 + 8 * i;
-          const bf16* g = dfull + (long long)(src[i] < 0 ? 0 : src[i]) * D + kc * 64 + c * 8;
+        for (int i = 0; i < NIT; ++i) {
+          const int r = r0 + RPP * i;
+          const bf16* g = dfull + (long long)(src[i] < 0 ? 0 : src[i]) * D + kc * 64 + c16 * 8;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + r * 128 + ((c ^ (r & 7)) << 4)),
                        "l"(g), "r"(src[i] < 0 ? 0 : 16)
                        : "memory");
@@ -210,17 +225,20 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
           mbar_wait(&acc1_empty[b], ((it >> 1) & 1) ^ 1);
           tc_after();
           const uint32_t d = tmem + b * 128;
-          for (int kc = 0; kc < nk; ++kc) {
+          for (int kc0 = 0; kc0 < nk; kc0 += RS_KPS) {
             mbar_wait(&a_full[as], aph);
-            mbar_wait(&w_full[ws], wph);
-            tc_after();
-            const uint64_t ad = sdesc(base + as * RS_CHUNK), bd = sdesc(base + RS_OFF_W + ws * RS_CHUNK);
+            for (int bk = 0; bk < RS_KPS; ++bk) {
+              const int kc = kc0 + bk;
+              mbar_wait(&w_full[ws], wph);
+              tc_after();
+              const uint64_t ad = sdesc(base + (as * RS_KPS + bk) * RS_CHUNK), bd = sdesc(base + RS_OFF_W + ws * RS_CHUNK);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mma_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+              for (int k = 0; k < 4; ++k) mma_ss(d, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+              mma_commit(&w_empty[ws]);
+              if (++ws == RS_WST) { ws = 0; wph ^= 1; }
+            }
             mma_commit(&a_empty[as]);
-            mma_commit(&w_empty[ws]);
             if (++as == RS_AST) { as = 0; aph ^= 1; }
-            if (++ws == RS_WST) { ws = 0; wph ^= 1; }
           }
           mma_commit(&acc1_full[b]);
         }
@@ -386,7 +404,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
 
 }  // namespace
 
-bool restore_supported(int D, int Hr) { return Hr == RS_HR && D % RS_NC == 0 && D >= RS_NC; }
+bool restore_supported(int D, int Hr) { return Hr == RS_HR && D % RS_NC == 0 && D % (64 * RS_KPS) == 0 && D >= RS_NC; }
 
 bool restore_make_maps(CUtensorMap* tmW1, CUtensorMap* tmW2, const bf16* Wr1, const bf16* Wr2, int D, int Hr,
                        char* err, size_t errlen) {
