@@ -271,7 +271,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
     const uint32_t ring = base + RS_OFF_EPI + (uint32_t)(warp - 4) * RS_RDEPTH * 4096;
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
-    constexpr int NSUB = 2;               // 32-column sub-chunks of a 128-column chunk per warp
+    // column sub-chunks of a 128-column chunk per warp: fp32 X 2 x 32 columns (128 B of a row);
+    // bf16 X one 64-column sub-chunk (also 128 B of a row), added in place in its ring slot
+    constexpr bool XB = sizeof(XT) == 2;
+    constexpr int NSUB = XB ? 1 : 2;
     int n2 = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int m = tile * RS_BM + q * 32 + lane;
@@ -288,15 +291,18 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
             const int rr = i * 4 + rsub;
             const int pr = __shfl_sync(0xffffffffu, prow, rr);
             const bool live = __shfl_sync(0xffffffffu, orow, rr) >= 0;
-            const uint32_t dst = ring + (uint32_t)(((cidx % RS_RDEPTH) * 32 + rr) * 128 + c4 * 4);
-            if constexpr (sizeof(XT) == 4)
+            if constexpr (!XB) {
+              const uint32_t dst = ring + (uint32_t)(((cidx % RS_RDEPTH) * 32 + rr) * 128 + c4 * 4);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
                            "l"(X + (long long)pr * D + col + c4), "r"(live ? 16 : 0)
                            : "memory");
-            else
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
-                           "l"(X + (long long)pr * D + col + c4), "r"(live ? 8 : 0)
+            } else {   // 16 B = 8 bf16 columns c8 = lane & 7, XOR-swizzled by row
+              const int c8 = lane & 7;
+              const uint32_t dst = ring + (uint32_t)(((cidx % RS_RDEPTH) * 32 + rr) * 128 + ((c8 ^ (rr & 7)) << 4));
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                           "l"(X + (long long)pr * D + col + c8 * 8), "r"(live ? 16 : 0)
                            : "memory");
+            }
           }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -340,19 +346,62 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
         }
         const int col = col_of(cidx);
         asm volatile("cp.async.wait_group %0;" ::"n"(RS_RDEPTH - 1) : "memory");
+        if constexpr (XB) {
+          // thread = row (TMEM lane 32q + lane): its 64 accumulators + b_r2 + its residual row
+          // segment (from the slot), rounded once to bf16 and written back in place; then 8
+          // lanes per row store the slot's rows coalesced
+          const uint32_t slot = ring + (uint32_t)((cidx % RS_RDEPTH) * 32 * 128);
+          __syncwarp();
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            float v[32];
+            tld32w(tq + 256 + b * 128 + half * 64 + h2 * 32, v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int ch = h2 * 4 + j;   // 16 B chunk of the row segment = columns 8 ch ..
+              const uint32_t a = slot + lane * 128 + ((ch ^ (lane & 7)) << 4);
+              uint32_t u[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]) : "r"(a) : "memory");
+              const float4 b0 = __ldg(reinterpret_cast<const float4*>(br2 + col + 8 * ch));
+              const float4 b1 = __ldg(reinterpret_cast<const float4*>(br2 + col + 8 * ch + 4));
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+              uint32_t o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x = unpack_bf16x2(u[e]);
+                o[e] = pack_bf16x2((v[8 * j + 2 * e] + bb[2 * e]) + x.x, (v[8 * j + 2 * e + 1] + bb[2 * e + 1]) + x.y);
+              }
+              sts128r(a, o[0], o[1], o[2], o[3]);
+            }
+          }
+          __syncwarp();
+          const int c8 = lane & 7;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + rsub;
+            const int orr = __shfl_sync(0xffffffffu, orow, rr);
+            uint32_t u[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                         : "r"(slot + rr * 128 + ((c8 ^ (rr & 7)) << 4))
+                         : "memory");
+            if (orr >= 0) *reinterpret_cast<uint4*>(X + (long long)orr * D + col + c8 * 8) = make_uint4(u[0], u[1], u[2], u[3]);
+          }
+          __syncwarp();
+          issue_resid(cidx + RS_RDEPTH);
+          if (cidx % NSUB == NSUB - 1) {
+            tc_before();
+            mbar_arrive(&acc2_empty[b]);
+            ++n2;
+          }
+          continue;
+        }
         float4 xc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int rr = i * 4 + rsub;
           const uint32_t a = ring + (uint32_t)(((cidx % RS_RDEPTH) * 32 + rr) * 128 + c4 * 4);
-          if constexpr (sizeof(XT) == 4) {
-            xc[i] = lds128r(a);
-          } else {
-            uint32_t u0, u1;
-            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(u0), "=r"(u1) : "r"(a) : "memory");
-            const float2 lo = unpack_bf16x2(u0), hi = unpack_bf16x2(u1);
-            xc[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
-          }
+          xc[i] = lds128r(a);
         }
         const uint32_t tile_u = ring + (uint32_t)((cidx % RS_RDEPTH) * 32 * 128);
         __syncwarp();   // every lane has its residual: the slot becomes the transpose tile
@@ -374,15 +423,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1)
           float4 v = make_float4(t4.x + bb.x, t4.y + bb.y, t4.z + bb.z, t4.w + bb.w);
           v.x += xc[i].x; v.y += xc[i].y; v.z += xc[i].z; v.w += xc[i].w;
           if (orr < 0) continue;
-          XT* o = X + (long long)orr * D + col + c4;
-          if constexpr (sizeof(XT) == 4) {
-            *reinterpret_cast<float4*>(o) = v;
-          } else {
-            uint2 u;
-            u.x = pack_bf16x2(v.x, v.y);
-            u.y = pack_bf16x2(v.z, v.w);
-            *reinterpret_cast<uint2*>(o) = u;
-          }
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(X) + (long long)orr * D + col + c4) = v;
         }
         __syncwarp();   // the slot's transpose reads are done before it is refilled
         issue_resid(cidx + RS_RDEPTH);

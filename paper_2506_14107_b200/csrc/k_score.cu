@@ -94,7 +94,37 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
     const XT* rp = past >= 0 ? X + ((long long)past * T + i) * D : nullptr;
     const XT* rf = fut >= 0 ? X + ((long long)fut * T + i) * D : nullptr;
     float cc = 0.f, pp = 0.f, ff = 0.f, cp = 0.f, cf = 0.f;
-    if constexpr (VPL > 0) {
+    if constexpr (VPL > 0 && sizeof(XT) == 2) {
+      // bf16 rows (RV_X_BF16): 16 B = 8 columns per load, VPL / 2 loads per row and lane
+      constexpr int V8 = VPL / 2;
+      const uint4* c16 = reinterpret_cast<const uint4*>(cur);
+      const uint4* p16 = reinterpret_cast<const uint4*>(rp ? rp : cur);
+      const uint4* f16 = reinterpret_cast<const uint4*>(rf ? rf : cur);
+      uint4 cv[V8], pv[V8], fv[V8];
+#pragma unroll
+      for (int j = 0; j < V8; ++j) {
+        cv[j] = __ldg(c16 + lane + 32 * j);
+        pv[j] = __ldg(p16 + lane + 32 * j);
+        fv[j] = __ldg(f16 + lane + 32 * j);
+      }
+#pragma unroll
+      for (int j = 0; j < V8; ++j) {
+        const uint32_t cu[4] = {cv[j].x, cv[j].y, cv[j].z, cv[j].w};
+        const uint32_t pu[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
+        const uint32_t fu[4] = {fv[j].x, fv[j].y, fv[j].z, fv[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 c = unpack_bf16x2(cu[e]), p = unpack_bf16x2(pu[e]), f = unpack_bf16x2(fu[e]);
+          cc += c.x * c.x + c.y * c.y;
+          pp += p.x * p.x + p.y * p.y;
+          cp += c.x * p.x + c.y * p.y;
+          ff += f.x * f.x + f.y * f.y;
+          cf += c.x * f.x + c.y * f.y;
+        }
+      }
+      if (!rp) pp = cp = 0.f;
+      if (!rf) ff = cf = 0.f;
+    } else if constexpr (VPL > 0) {
       const XT* rp2 = rp ? rp : cur;
       const XT* rf2 = rf ? rf : cur;
       float4 cv[VPL], pv[VPL], fv[VPL];
@@ -168,6 +198,24 @@ __global__ void __launch_bounds__(SCORE_THREADS, RV_SCORE_MINB)
       // Eq. 8: Delta R_i = R_cur_i - R_ref_i, written now while both rows are cache-hot, to
       // the wave-local token row w*T + i: the restoration GEMM reads it there in place
       const XT* rr = prov ? rf : rp;
+      if constexpr (sizeof(XT) == 2) {   // bf16 rows: 8 columns (16 B in, 16 B out) per lane step
+        const uint4* a16 = reinterpret_cast<const uint4*>(cur);
+        const uint4* b16 = reinterpret_cast<const uint4*>(rr);
+        uint4* o16 = reinterpret_cast<uint4*>(dfull + ((long long)w * T + i) * D);
+#pragma unroll 4
+        for (int k = lane; k < (D >> 3); k += 32) {
+          const uint4 a = __ldg(a16 + k), b = __ldg(b16 + k);
+          const uint32_t au[4] = {a.x, a.y, a.z, a.w}, bu[4] = {b.x, b.y, b.z, b.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 x = unpack_bf16x2(au[e]), y = unpack_bf16x2(bu[e]);
+            o[e] = pack_bf16x2(x.x - y.x, x.y - y.y);
+          }
+          o16[k] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        continue;
+      }
       uint2* o = reinterpret_cast<uint2*>(dfull + ((long long)w * T + i) * D);
 #pragma unroll 4
       for (int k = lane; k < D4; k += 32) {
