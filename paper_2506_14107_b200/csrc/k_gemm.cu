@@ -204,7 +204,9 @@ RV_DEV float quick_gelu_fast(float x) {
   return x * fmaf(0.5f, t, 0.5f);
 }
 
-template <int BN, int MODE, bool PAIR>
+// RB16: the residual rows are bf16 (RV_X_BF16), a separate instantiation so that the fp32
+// residual path's register allocation is untouched
+template <int BN, int MODE, bool PAIR, bool RB16 = false>
 __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const int* __restrict__ M_dev, int M_host, int N, int K, const Epi e) {
@@ -354,6 +356,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
       // Residual rows are known before the accumulator is: load chunk c+1's residual while
       // chunk c is processed (8 x 16 B in flight per lane; the first batch overlaps the MMA).
       float4 xn[8];
+      uint2 rn16[RB16 ? 8 : 1];   // RE + bf16 residual: the next chunk's rows, loaded with this chunk's
+      auto load_resid16 = [&](int c, uint2* x) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 4 + rsub;
+          const long long off = (long long)rrow_s[rr] * e.resid_ld + nb * BN + c * 32 + c4;
+          x[i] = (rr < nvalid && orow_s[rr] >= 0) ? *reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.resid) + off)
+                                                  : make_uint2(0u, 0u);
+        }
+      };
       auto load_resid = [&](int c, float4 (&x)[8]) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -361,7 +373,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
           const long long off = (long long)rrow_s[rr] * e.resid_ld + nb * BN + c * 32 + c4;
           if (!(rr < nvalid && orow_s[rr] >= 0)) {
             x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else if (e.resid_bf16) {
+          } else if constexpr (RB16) {
             const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(e.resid) + off);
             const float2 lo = unpack_bf16x2(u.x), hi = unpack_bf16x2(u.y);
             x[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
             const int rrow = __shfl_sync(0xffffffffu, rrow_reg, live ? rr : 0);
             const long long off = (long long)rrow * e.resid_ld + nb * BN + c * 32 + c4;
             const uint32_t dst = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
-            if (e.resid_bf16)   // 4 bf16 = 8 B into the first half of the lane's 16 B chunk
+            if constexpr (RB16)   // 4 bf16 = 8 B into the first half of the lane's 16 B chunk
               asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst),
                            "l"(reinterpret_cast<const bf16*>(e.resid) + off), "r"(live ? 8 : 0)
                            : "memory");
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
             for (int i = 0; i < 8; ++i) {
               const int rr = i * 4 + rsub;
               const uint32_t a = ring + (uint32_t)(((c % RDEPTH) * 32 + rr) * 128 + c4 * 4);
-              if (e.resid_bf16) {
+              if constexpr (RB16) {
                 uint32_t u0, u1;
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(u0), "=r"(u1) : "r"(a) : "memory");
                 const float2 lo = unpack_bf16x2(u0), hi = unpack_bf16x2(u1);
@@ -433,7 +445,27 @@ __global__ void __launch_bounds__(gemm_threads<BN, MODE>(), 1)
         } else {
           // RE: twice the warps hide the latency; this chunk's residual loads overlap the
           // TMEM load and the transpose below (no register prefetch: 96 registers per thread)
-          if (e.resid) load_resid(c, xc);
+          if (RB16 && e.resid) {
+            // bf16 rows: 32 columns are 64 B, half a line; the warp's next chunk holds the other
+            // half, so both chunks' loads are issued together (one 128 B access per row instead
+            // of two 64 B ones apart in time) and the next chunk's wait in registers (16)
+            uint2 cur16[8];
+            if (c == c_beg) {
+              load_resid16(c, cur16);
+              if (c + 1 < c_end) load_resid16(c + 1, rn16);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cur16[i] = rn16[i];
+              if (c + 1 < c_end) load_resid16(c + 1, rn16);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float2 lo = unpack_bf16x2(cur16[i].x), hi = unpack_bf16x2(cur16[i].y);
+              xc[i] = make_float4(lo.x, lo.y, hi.x, hi.y);
+            }
+          } else if (e.resid) {
+            load_resid(c, xc);
+          }
         }
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, r);
@@ -535,23 +567,23 @@ bool encode_2d(CUtensorMap* m, const void* ptr, long long rows, int cols, int bo
 
 int num_sms() { return dev_sms(); }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool RB16 = false>
 cudaError_t launch_mode(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
   using C = Cfg<BN, MODE>;
-  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, false>>(C::SMEM);
+  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, false, RB16>>(C::SMEM);
   if (err != cudaSuccess) return err;
   const int tiles = ((max_m + BM - 1) / BM) * (p.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, MODE, false><<<grid, gemm_threads<BN, MODE>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
+  gemm_tc_kernel<BN, MODE, false, RB16><<<grid, gemm_threads<BN, MODE>(), C::SMEM, s>>>(p.tmA, p.tmB, M_dev, M_host, p.N, p.K, e);
   return cudaGetLastError();
 }
 
 // CTA-pair launch: clusters of 2 (one TPC), grid = 2 x min(tiles, SMs / 2)
-template <int BN, int MODE>
+template <int BN, int MODE, bool RB16 = false>
 cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max_m, const Epi& e, cudaStream_t s) {
   using C = Cfg<BN, MODE, true>;
-  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, true>>(C::SMEM);
+  cudaError_t err = ensure_smem<gemm_tc_kernel<BN, MODE, true, RB16>>(C::SMEM);
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(gemm_threads<BN, MODE>());
@@ -571,7 +603,7 @@ cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max
   if (!max_pairs) {
     cfg.gridDim = dim3(num_sms() & ~1);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, MODE, true>, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<BN, MODE, true, RB16>, &cfg) != cudaSuccess || n < 1) {
       cudaGetLastError();
       n = num_sms() / 2;
     }
@@ -583,7 +615,7 @@ cudaError_t launch_pair(const GemmPlan& p, const int* M_dev, int M_host, int max
   if (tiles < pairs) pairs = tiles;
   if (pairs < 1) pairs = 1;
   cfg.gridDim = dim3(2 * pairs);
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE, true>, p.tmA, p.tmB2, M_dev, M_host, p.N, p.K, e);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, MODE, true, RB16>, p.tmA, p.tmB2, M_dev, M_host, p.N, p.K, e);
 }
 
 #ifndef RV_GEMM_RE
@@ -605,7 +637,9 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   // W_o 193 -> 154; in the bench FC2 67 -> 60 ms per step); R1 (N = 128) stays single-CTA
   // (17 -> 20 ms as pairs: half as many 256-row tiles on small waves)
   constexpr bool pair_on = RV_GEMM_PAIR != 0;
-  if (p.K <= 2 * BK && e.resid) return launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
+  if (p.K <= 2 * BK && e.resid)
+    return e.resid_bf16 ? launch_mode<BN, 1, true>(p, M_dev, M_host, max_m, e, s)
+                        : launch_mode<BN, 1>(p, M_dev, M_host, max_m, e, s);
 // RV_GEMM_RE_KMAX: largest K that takes the 16-warp epilogue (MODE 2).  FC2 (K = 4096) as MODE 2
 // pairs: 70.1 vs 60.8 ms per step as MODE 0 pairs (fewer stages for its long mainloop)
 #ifndef RV_GEMM_RE_KMAX
@@ -614,7 +648,8 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   if constexpr (BN == 256) {
     if (pair_on) {
       if (re_on && p.K <= RV_GEMM_RE_KMAX && (e.resid ? BN >= 128 : BN == 256))
-        return launch_pair<BN, 2>(p, M_dev, M_host, max_m, e, s);
+        return (e.resid && e.resid_bf16) ? launch_pair<BN, 2, true>(p, M_dev, M_host, max_m, e, s)
+                                         : launch_pair<BN, 2>(p, M_dev, M_host, max_m, e, s);
       return launch_pair<BN, 0>(p, M_dev, M_host, max_m, e, s);
     }
   }
@@ -622,8 +657,10 @@ cudaError_t launch_bn(const GemmPlan& p, const int* M_dev, int M_host, int max_m
   // K <= 1024 (QKV with its K/V scatter, FC1 with QuickGELU: 65 -> 57 and 82 -> 73 ms per step);
   // not R1 (N = 128: one N tile, slower)
   if (re_on && p.K <= 1024 && (e.resid ? BN >= 128 : BN == 256))
-    return launch_mode<BN, 2>(p, M_dev, M_host, max_m, e, s);
-  return launch_mode<BN, 0>(p, M_dev, M_host, max_m, e, s);
+    return (e.resid && e.resid_bf16) ? launch_mode<BN, 2, true>(p, M_dev, M_host, max_m, e, s)
+                                     : launch_mode<BN, 2>(p, M_dev, M_host, max_m, e, s);
+  return (e.resid && e.resid_bf16) ? launch_mode<BN, 0, true>(p, M_dev, M_host, max_m, e, s)
+                                   : launch_mode<BN, 0>(p, M_dev, M_host, max_m, e, s);
 }
 
 }  // namespace
