@@ -46,6 +46,8 @@ def classify(names):
             out.append("rgather")
         elif "attn" in n:
             out.append("attention")
+        elif "restore_kernel" in n:
+            out.append("restore")
         elif "gemm_tc_kernel" in n:
             if gi is None:
                 out.append("gemm_pe")
