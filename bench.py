@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--attn-sync", action="store_true", help="mma.sync attention kernel (RV_ATTN_SYNC) instead of tcgen05")
     ap.add_argument("--chain", action="store_true", help="SPEC chain variant (RV_CHAIN, SURVEY NEXT-1) instead of D1")
     ap.add_argument("--x-bf16", action="store_true", help="experimental bf16 residual stream (RV_X_BF16)")
+    ap.add_argument("--restore-gemms", action="store_true", help="diagnostic: restoration as two GEMMs (RV_RESTORE_GEMMS)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: the 7,200-frame L/14 video (default); c5: L/14@336 multi-video, LPT-sharded")
@@ -350,7 +351,7 @@ def main():
 
     def step(profile):
         m.embed_async(x, c, plan, out=(emb, masks, None), stream=stream, profile=profile, attn_tc=not args.attn_sync,
-                      chain=args.chain, x_bf16=args.x_bf16)
+                      chain=args.chain, x_bf16=args.x_bf16, restore_gemms=args.restore_gemms)
         st = m.wait()
         if world > 1:     # NCCL over NVLink only to gather embeddings + masks
             gather_rows([emb, masks.view(n_loc, -1)], counts)

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <string>
 #include <vector>
+#include <chrono>
 
 #include "../../include/reusevit.h"
 #include "../../include/reusevit_stages.h"
@@ -155,6 +156,8 @@ struct rv_ctx {
   bool inflight = false;
   int cur_n = 0, cur_nonI = 0, cur_levels = 0, cur_launches = 0;
   uint32_t cur_flags = 0;
+  std::vector<long long> wf_sig;   // wave structure of the last wavefront decision, and its R
+  int wf_R_last = 0;
   cudaStream_t cur_stream = nullptr;
   std::vector<Wave> waves;
   std::vector<int> wdesc_host;
@@ -317,6 +320,7 @@ void release_wavefront(rv_ctx* ctx) {
   if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
   free_list(ctx->wfallocs);
   ctx->wf_key.clear();
+  ctx->wf_sig.clear();
   ctx->Xr.clear(); ctx->KVr.clear(); ctx->KSr.clear(); ctx->tmKVr.clear(); ctx->wbuf.clear();
   ctx->wf_bytes = ctx->wf_cache_bytes = 0;
 }
@@ -1235,6 +1239,10 @@ rv_status rv_load_gates(rv_ctx* ctx, const float* blob, size_t n_floats) {
 rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const rv_plan* plan, uint32_t flags,
                    void* cuda_stream, float* emb, uint8_t* masks, float* scores) {
   if (!ctx) return RV_ECONTRACT;
+#ifdef RV_HOST_TIMING   // experiment builds only: host time of rv_embed's phases on stderr
+  const auto ht0 = std::chrono::steady_clock::now();
+  auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ht0).count(); };
+#endif
   if (ctx->inflight) return fail(ctx, RV_EBUSY, "rv_embed: an embed is already in flight");
   if (!ctx->vit_loaded) return fail(ctx, RV_ECONTRACT, "rv_embed: ViT weights not loaded");
   const bool dense = flags & RV_DENSE;
@@ -1294,10 +1302,24 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
   // free device memory (the rest is left to the caller, e.g. a second pipelined context).
   // Profiled, ablation and chain embeds keep the serial level order.
   ctx->wf_R = 0;
-  if (!(flags & (RV_SERIAL_WAVES | RV_PROFILE | RV_KEEP_ALL_CACHE | RV_CHAIN | RV_WAVE_FRAME)) &&
-      ctx->waves.size() >= 2 && max_w <= kWavefrontMaxWave) {
+  // the ring size is re-decided only when the wave structure or the buffers changed: the free
+  // memory query behind it occasionally stalls the host for milliseconds (measured up to 7 ms on
+  // a 2.5 ms clip), so repeated embeds of the same shape reuse the previous decision
+  std::vector<long long> wf_sig = {(long long)ctx->n_cap, ctx->capC, ctx->capR};
+  for (const Wave& w : ctx->waves) wf_sig.push_back(w.n_w * 2 + (w.any_ref ? 1 : 0));
+  const bool wf_want = !(flags & (RV_SERIAL_WAVES | RV_PROFILE | RV_KEEP_ALL_CACHE | RV_CHAIN | RV_WAVE_FRAME)) &&
+                       ctx->waves.size() >= 2 && max_w <= kWavefrontMaxWave;
+  if (wf_want && wf_sig == ctx->wf_sig && ctx->wf_R_last >= 3 && ensure_wavefront(ctx, ctx->wf_R_last) == RV_OK) {
+    ctx->wf_R = ctx->wf_R_last;
+  } else if (wf_want) {
     size_t fr = 0, tot = 0;
+#ifdef RV_HOST_TIMING
+    const double ht_m0 = hms();
+#endif
     CK(cudaMemGetInfo(&fr, &tot));
+#ifdef RV_HOST_TIMING
+    fprintf(stderr, "  memgetinfo %.3f ms (at %.3f)\n", hms() - ht_m0, ht_m0);
+#endif
     const unsigned long long avail = fr + ctx->wf_bytes, reserve = 4ull << 30;
     const unsigned long long budget = avail > reserve ? (avail - reserve) / 2 : 0;
     int R = std::min(L + 1, (int)ctx->waves.size() + 1);
@@ -1310,6 +1332,8 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
         ctx->err.clear();
       }
     }
+    ctx->wf_sig = wf_sig;
+    ctx->wf_R_last = ctx->wf_R;
   }
   if (flags & RV_CHAIN) {
     if ((st = ensure_chain_buffers(ctx, n))) return st;
@@ -1350,8 +1374,14 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
     CK(cudaStreamWaitEvent(ws, ctx->ev[3], 0));
   }
   CK(cudaEventRecord(ctx->ev[0], ws));
+#ifdef RV_HOST_TIMING
+  const double ht_c0 = hms();
+#endif
   CK(cudaMemcpyAsync(ctx->wdesc, ctx->wdesc_host.data(), ctx->wdesc_host.size() * sizeof(int),
                      cudaMemcpyHostToDevice, ws));
+#ifdef RV_HOST_TIMING
+  fprintf(stderr, "  wdesc copy %.3f ms (at %.3f)\n", hms() - ht_c0, ht_c0);
+#endif
   if (flags & RV_CHAIN) {   // wave row map, query offsets, identity source rows of layer 1's q|k|v
     CK(cudaMemcpyAsync(ctx->wrows, ctx->wrows_host.data(), ctx->wrows_host.size() * sizeof(int),
                        cudaMemcpyHostToDevice, ws));
@@ -1367,6 +1397,10 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
       CK(cudaMemcpyAsync(ctx->out_masks, masks, (size_t)n * L * N, cudaMemcpyHostToDevice, ws));
   }
   CK(cudaEventRecord(ctx->ev[1], ws));
+#ifdef RV_HOST_TIMING
+  const double ht_pre = hms();
+  bool ht_cap = false;
+#endif
   // ---- compute: cached CUDA graph keyed on everything the recorded sequence depends on
   std::vector<long long> key = {(long long)n, (long long)(flags & ~RV_NO_GRAPH), (long long)(intptr_t)d_patches,
                                 (long long)(intptr_t)d_codec, (long long)(intptr_t)d_emb,
@@ -1383,6 +1417,9 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
     if (rec.err != cudaSuccess) return fail(ctx, RV_ECUDA, "launch %s: %s", rec.where, cudaGetErrorString(rec.err));
   } else {
     if (!ctx->gexec || key != ctx->gkey) {
+#ifdef RV_HOST_TIMING
+      ht_cap = true;
+#endif
       if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
       cudaGraph_t g = nullptr;
       ctx->prof_used = 0;
@@ -1402,7 +1439,14 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
       ctx->gkey = key;
       ctx->cur_launches = rec.launches;
     }
+#ifdef RV_HOST_TIMING
+    const double ht_l0 = hms();
+#endif
     CK(cudaGraphLaunch(ctx->gexec, ws));
+#ifdef RV_HOST_TIMING
+    fprintf(stderr, "rv_embed host: pre %.3f ms, capture %d, to launch %.3f, launch %.3f ms\n", ht_pre, (int)ht_cap,
+            ht_l0, hms() - ht_l0);
+#endif
     rec.launches = ctx->cur_launches;
   }
   CK(cudaEventRecord(ctx->ev[2], ws));
