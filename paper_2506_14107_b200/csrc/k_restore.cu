@@ -457,25 +457,17 @@ cudaError_t launch_restore(const CUtensorMap& tmW1, const CUtensorMap& tmW2, con
                            const int* provrow, const int* idxR, const int* M_dev, int max_rows, const float* br1,
                            const float* br2, void* X, int x_bf16, int D, cudaStream_t s) {
   if (max_rows <= 0) return cudaSuccess;
-  const int dev = cur_device();
-  static bool attr[64][2] = {};
   const int sms = dev_sms();
   const int tiles = (max_rows + RS_BM - 1) / RS_BM;
   const int grid = tiles < sms ? tiles : sms;
   if (x_bf16) {
-    if (!attr[dev & 63][1]) {
-      cudaError_t e = cudaFuncSetAttribute(restore_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SMEM);
-      if (e != cudaSuccess) return e;
-      attr[dev & 63][1] = true;
-    }
+    cudaError_t e = ensure_smem<restore_kernel<bf16>>(RS_SMEM);
+    if (e != cudaSuccess) return e;
     restore_kernel<bf16><<<grid, RS_THREADS, RS_SMEM, s>>>(tmW1, tmW2, dfull, rloc, provrow, idxR, M_dev, br1, br2,
                                                             reinterpret_cast<bf16*>(X), D);
   } else {
-    if (!attr[dev & 63][0]) {
-      cudaError_t e = cudaFuncSetAttribute(restore_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RS_SMEM);
-      if (e != cudaSuccess) return e;
-      attr[dev & 63][0] = true;
-    }
+    cudaError_t e = ensure_smem<restore_kernel<float>>(RS_SMEM);
+    if (e != cudaSuccess) return e;
     restore_kernel<float><<<grid, RS_THREADS, RS_SMEM, s>>>(tmW1, tmW2, dfull, rloc, provrow, idxR, M_dev, br1, br2,
                                                              reinterpret_cast<float*>(X), D);
   }
