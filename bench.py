@@ -458,10 +458,73 @@ def main():
             del m2
         except RuntimeError as ex:      # e.g. not enough HBM for a second context
             print(f"[bench] pipelined e2e skipped: {ex}", file=sys.stderr)
-        ems = ems_pipe if ems_pipe is not None else ems_serial
+        # streamed: one context; every step's inputs are copied from pinned host memory into one
+        # of two device staging buffers on a copy stream (step k+1's H2D overlaps step k's
+        # compute; a staging buffer is refilled only after its contents moved on), moved into the
+        # embed's fixed input buffers on the compute stream (device to device, so the cached
+        # graph keeps its input pointers), embedded there (RV_DEVICE_PTRS), and the embeddings
+        # and masks are read back to pinned host memory every step; embeds never overlap
+        ems_stream = None
+        try:
+            xs = [torch.empty_like(x), torch.empty_like(x)]
+            cst = [torch.empty_like(c), torch.empty_like(c)]
+            xf, cf = torch.empty_like(x), torch.empty_like(c)
+            ed = torch.empty((n_loc, D), dtype=torch.float32, device=dev)
+            md = torch.empty((n_loc, L, N), dtype=torch.uint8, device=dev)
+            eh, mh, _ = host_outs()
+            eh_t, mh_t = torch.from_numpy(eh), torch.from_numpy(mh)
+            cs = torch.cuda.Stream(dev)
+            ready = [torch.cuda.Event(), torch.cuda.Event()]
+            moved = [torch.cuda.Event(), torch.cuda.Event()]
+
+            def h2d_copy(k):
+                with torch.cuda.stream(cs):
+                    if k >= 2:
+                        cs.wait_event(moved[k % 2])
+                    xs[k % 2].copy_(xh, non_blocking=True)
+                    cst[k % 2].copy_(ch, non_blocking=True)
+                    ready[k % 2].record(cs)
+
+            def sstep(k, last):
+                stream.wait_event(ready[k % 2])
+                with torch.cuda.stream(stream):
+                    xf.copy_(xs[k % 2], non_blocking=True)
+                    cf.copy_(cst[k % 2], non_blocking=True)
+                moved[k % 2].record(stream)
+                m.embed_async(xf, cf, plan, out=(ed, md, None), stream=stream, **variant)
+                if not last:            # after the embed's own (small) launches are queued
+                    h2d_copy(k + 1)
+                with torch.cuda.stream(stream):
+                    eh_t.copy_(ed, non_blocking=True)
+                    mh_t.copy_(md, non_blocking=True)
+                m.wait()
+            h2d_copy(0)                 # warm-up (graph capture for the device-pointer inputs)
+            sstep(0, True)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            cs.wait_event(s0)
+            h2d_copy(0)
+            for k in range(args.steps):
+                sstep(k, k == args.steps - 1)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            ems_stream = max_over_ranks(s0.elapsed_time(s1) / args.steps)
+            del xs, cst, xf, cf
+        except RuntimeError as ex:      # e.g. not enough HBM for the staging buffers
+            print(f"[bench] streamed e2e skipped: {ex}", file=sys.stderr)
+        modes = {"serial": ems_serial}
+        if ems_pipe is not None:
+            modes["pipelined, 2 contexts / 2 streams"] = ems_pipe
+        if ems_stream is not None:
+            modes["streamed, 1 context, double-buffered device inputs on a copy stream"] = ems_stream
+        mode = min(modes, key=modes.get)
+        ems = modes[mode]
         e2e = {"value": n_total / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "mode": "pipelined, 2 contexts / 2 streams" if ems_pipe is not None else "serial",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "mode": mode,
+               "by_mode": {k: n_total / (v / 1e3) for k, v in modes.items()},
                "serial_value": n_total / (ems_serial / 1e3)}
         del xh, ch
 

@@ -318,14 +318,42 @@ __global__ void __launch_bounds__(COMPACT_THREADS)
   }
 }
 
+// zero n 32-bit words (a kernel, not a memset node: the embed graph then holds no copy-engine
+// work that a concurrent host-to-device copy of the next inputs could delay)
+__global__ void zero_words_kernel(uint32_t* __restrict__ p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+
+__global__ void iota_kernel(int* __restrict__ p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = (int)i;
+}
+
 }  // namespace
+
+cudaError_t launch_iota(int* p, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long long g = (n + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  iota_kernel<<<(int)g, 256, 0, s>>>(p, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_words(void* p, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long long g = (n + 255) / 256;
+  if (g > 148) g = 148;
+  zero_words_kernel<<<(int)g, 256, 0, s>>>(reinterpret_cast<uint32_t*>(p), n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, int layer, int n_w, const int* wdesc,
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
                          int* cntR, bf16* dfull, cudaStream_t s) {
   if (n_w <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(cntR, 0, (size_t)n_w * sizeof(int), s);
+  cudaError_t e = launch_zero_words(cntR, n_w, s);
   if (e != cudaSuccess) return e;
   int tok = SCORE_TOK;
   while (tok > SCORE_THREADS / 32 && (long long)n_w * ((N + tok - 1) / tok) < 3LL * dev_sms()) tok >>= 1;

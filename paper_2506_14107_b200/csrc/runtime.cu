@@ -124,7 +124,7 @@ struct rv_ctx {
   float* pcl2 = nullptr;               // second CLS-attention buffer (t of the next decision)
   int* wrows = nullptr;                // [n][T] global row f*T+i of every wave-local token, desc order
   int* qoffT = nullptr;                // [n+1] w*T (all T tokens of a frame are queries)
-  std::vector<int> wrows_host, iota_host, qoffT_host;
+  std::vector<int> wrows_host, qoffT_host;
   // GEMM plans (tensor maps) bound to the buffers above
   GemmPlan pe;
   CUtensorMap tmQ;                 // q buffer [capC][D], box {64, 64} (tcgen05 attention)
@@ -156,6 +156,9 @@ struct rv_ctx {
   bool inflight = false;
   int cur_n = 0, cur_nonI = 0, cur_levels = 0, cur_launches = 0;
   uint32_t cur_flags = 0;
+  std::vector<int> wdesc_dev_copy;  // what ctx->wdesc holds on the device (cleared on realloc)
+  std::vector<int> chain_dev_copy;  // the plan the chain maps (wrows, qoffT) were uploaded for
+  const int* chain_dev_ptr = nullptr;
   std::vector<long long> wf_sig;   // wave structure of the last wavefront decision, and its R
   int wf_R_last = 0;
   cudaStream_t cur_stream = nullptr;
@@ -334,6 +337,7 @@ void release_buffers(rv_ctx* ctx) {
   ctx->Xall = nullptr; ctx->KVall = nullptr; ctx->keepall = false; ctx->tmKVl.clear();
   ctx->cache_bytes = ctx->alloc_bytes = 0;
   ctx->dfull = nullptr; ctx->rpos = nullptr; ctx->rloc = nullptr; ctx->patches_bf16 = nullptr; ctx->wdesc = nullptr;
+  ctx->wdesc_dev_copy.clear();
   ctx->wmask = ctx->wprov = nullptr;
   ctx->cntR = ctx->idxC = ctx->idxR = ctx->provrow = ctx->qoff = ctx->counts = nullptr;
   ctx->A = ctx->q = ctx->att = ctx->h = ctx->hr = nullptr; ctx->x1 = nullptr; ctx->reuse_ctr = nullptr;
@@ -616,8 +620,7 @@ void record_embed(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float* patch
   // RV_X_BF16: the residual stream X (every layer's input/output rows) is stored in bf16; the X
   // buffers keep their fp32 size and hold the bf16 rows in their first half-rows
   const int xb = (flags & RV_X_BF16) ? 1 : 0;
-  r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
-  --r.launches;
+  r.chk(launch_zero_words(ctx->reuse_ctr, 128, s), "zero reuse counters");
   // a1: patch embed (dense, all frames): bf16 operand, GEMM into X0 rows f*T+1+i, finish.
   r.begin(K_PATCH,-1,-1);
   r.chk(launch_patch_to_bf16(patches, ctx->patches_bf16, (long long)n * N, ctx->pp, ctx->KP, s), "patch_to_bf16");
@@ -845,8 +848,7 @@ void record_embed_chain(rv_ctx* ctx, Rec& r, int n, uint32_t flags, const float*
   const bool dense = flags & RV_DENSE;
   const bool force = flags & RV_FORCE_MASKS;
   const long long ld3 = 3LL * D;
-  r.chk(cudaMemsetAsync(ctx->reuse_ctr, 0, 64 * sizeof(unsigned long long), s), "memset");
-  --r.launches;
+  r.chk(launch_zero_words(ctx->reuse_ctr, 128, s), "zero reuse counters");
   r.begin(K_PATCH,-1,-1);
   r.chk(launch_patch_to_bf16(patches, ctx->patches_bf16, (long long)n * N, ctx->pp, ctx->KP, s), "patch_to_bf16");
   {
@@ -1341,8 +1343,6 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
     ctx->wrows_host.resize((size_t)nd * T);
     for (int k = 0; k < nd; ++k)
       for (int i = 0; i < T; ++i) ctx->wrows_host[(size_t)k * T + i] = ctx->wdesc_host[(size_t)k * 4] * T + i;
-    ctx->iota_host.resize((size_t)n * T);
-    for (size_t i = 0; i < ctx->iota_host.size(); ++i) ctx->iota_host[i] = (int)i;
     ctx->qoffT_host.resize((size_t)n + 1);
     for (int w = 0; w <= n; ++w) ctx->qoffT_host[w] = w * T;
   }
@@ -1377,18 +1377,29 @@ rv_status rv_embed(rv_ctx* ctx, const float* patches, const float* codec, const 
 #ifdef RV_HOST_TIMING
   const double ht_c0 = hms();
 #endif
-  CK(cudaMemcpyAsync(ctx->wdesc, ctx->wdesc_host.data(), ctx->wdesc_host.size() * sizeof(int),
-                     cudaMemcpyHostToDevice, ws));
+  // the wave descriptors change only with the plan: re-uploading them every call put a small
+  // host-to-device copy into the copy-engine queue behind whatever the caller streams in
+  // concurrently (the next step's inputs), stalling this embed until that copy finished
+  if (ctx->wdesc_dev_copy != ctx->wdesc_host) {
+    CK(cudaMemcpyAsync(ctx->wdesc, ctx->wdesc_host.data(), ctx->wdesc_host.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ws));
+    ctx->wdesc_dev_copy = ctx->wdesc_host;
+  }
 #ifdef RV_HOST_TIMING
   fprintf(stderr, "  wdesc copy %.3f ms (at %.3f)\n", hms() - ht_c0, ht_c0);
 #endif
   if (flags & RV_CHAIN) {   // wave row map, query offsets, identity source rows of layer 1's q|k|v
-    CK(cudaMemcpyAsync(ctx->wrows, ctx->wrows_host.data(), ctx->wrows_host.size() * sizeof(int),
-                       cudaMemcpyHostToDevice, ws));
-    CK(cudaMemcpyAsync(ctx->qoffT, ctx->qoffT_host.data(), ctx->qoffT_host.size() * sizeof(int),
-                       cudaMemcpyHostToDevice, ws));
-    CK(cudaMemcpyAsync(ctx->kvsrc, ctx->iota_host.data(), ctx->iota_host.size() * sizeof(int),
-                       cudaMemcpyHostToDevice, ws));
+    // (the maps follow the plan and are uploaded when it or the buffers change; the identity
+    // rows are rewritten every call by a kernel, since the embed overwrites them)
+    if (ctx->chain_dev_copy != ctx->wdesc_host || ctx->chain_dev_ptr != ctx->wrows) {
+      CK(cudaMemcpyAsync(ctx->wrows, ctx->wrows_host.data(), ctx->wrows_host.size() * sizeof(int),
+                         cudaMemcpyHostToDevice, ws));
+      CK(cudaMemcpyAsync(ctx->qoffT, ctx->qoffT_host.data(), ctx->qoffT_host.size() * sizeof(int),
+                         cudaMemcpyHostToDevice, ws));
+      ctx->chain_dev_copy = ctx->wdesc_host;
+      ctx->chain_dev_ptr = ctx->wrows;
+    }
+    CK(launch_iota(ctx->kvsrc, (long long)n * T, ws));
   }
   if (!devp) {
     CK(cudaMemcpyAsync(ctx->in_patches, patches, (size_t)n * N * ctx->pp * 4, cudaMemcpyHostToDevice, ws));

@@ -67,6 +67,8 @@ cudaError_t launch_score(const void* X, int x_bf16, int T, int D, int N, int L, 
                          const float* tsrc, int tH, const float* codec, const uint8_t* force, const float* gate,
                          int Hg, int dense, uint8_t* masks, float* scores, uint8_t* wmask, uint8_t* wprov,
                          int* cntR, bf16* dfull, cudaStream_t s);
+cudaError_t launch_zero_words(void* p, long long n_words, cudaStream_t s);
+cudaError_t launch_iota(int* p, long long n, cudaStream_t s);   // p[i] = i
 cudaError_t launch_compact(int n_w, int T, const int* wdesc, const uint8_t* wmask, const uint8_t* wprov,
                            const int* cntR, int* idxC, int* idxR, int* provrow, int* qoff, int* counts, int* kvsrc,
                            unsigned long long* reuse_ctr, int* count_log, int* rpos, int* rloc, cudaStream_t s,
