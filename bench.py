@@ -583,10 +583,17 @@ def main():
                                if dom["flops"] > 0 else None)}
     gemm_ms = sum(p["ms"] for p in prof if p["name"].startswith("gemm"))
     gemm_fl = sum(p["flops"] for p in prof if p["name"].startswith("gemm"))
-    kernels = [{"name": p["name"], "launches": p["launches"], "ms": round(p["ms"], 3),
-                "share": round(p["ms"] / prof_step_ms, 4),
-                ("tflops" if p["flops"] > 0 else "gbs"): round((p["flops"] / 1e12 if p["flops"] > 0 else p["bytes"] / 1e9)
-                                                               / max(p["ms"], 1e-9) * 1e3, 1)} for p in prof]
+    # per class: TF/s of its tensor FLOPs and GB/s of its algorithmic bytes, each
+    # where the class has them (attention, W_o and the restoration have both)
+    kernels = []
+    for p in prof:
+        kr = {"name": p["name"], "launches": p["launches"], "ms": round(p["ms"], 3),
+              "share": round(p["ms"] / prof_step_ms, 4)}
+        if p["flops"] > 0:
+            kr["tflops"] = round(p["flops"] / 1e12 / max(p["ms"], 1e-9) * 1e3, 1)
+        if p["bytes"] > 0:
+            kr["gbs"] = round(p["bytes"] / 1e9 / max(p["ms"], 1e-9) * 1e3, 1)
+        kernels.append(kr)
 
     # ---- CPU oracle on a bounded sample + parity of the same frames
     cpu = None
