@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128)
   int* rows_s = reinterpret_cast<int*>(Qs + QT * KS);  // [Tp] K/V source row of every key
   float* scls = reinterpret_cast<float*>(rows_s + Tp); // [Tp] raw CLS logits (q_cls . k_j)
   __shared__ float s_cls[2];                          // CLS row max / sum
-  const long long ld = kv_ld;       // K/V cache row stride: 2D ([k | v]) or 3D ([k | v | q], chain variant)
+  const long long ld = kv_ld;       // K/V cache row stride: 2D ((k_h v_h) per head) or 3D (+ q, chain variant)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;

@@ -98,7 +98,7 @@ cudaError_t launch_attention_tc(const CUtensorMap& tmQ, const CUtensorMap& tmKV,
 // q_mode 0: compacted queries q[qoff[w] + r], loaded through tmQ (box {64, 64} over q, row stride
 // q_ld = D); 1: every token of a frame is a query with its q row q[kvsrc[slot T + i]] at column
 // q_col (chain variant's q|k|v cache, tmQ unused); K / V rows through kvsrc (identity if null)
-// with stride kv_ld (K at column h d_h, V at D + h d_h); output rows qoff[w] + r.
+// with stride kv_ld (head h: K at column 2 h d_h, V at 2 h d_h + d_h); output rows qoff[w] + r.
 bool attn_tcg_supported(int T, int D, int H);
 cudaError_t launch_attention_tcg(const CUtensorMap* tmQ, const bf16* q, long long q_ld, int q_col, int q_mode,
                                  const bf16* KV, long long kv_ld, const int* kvsrc, bf16* out, const int* wdesc,
